@@ -1,0 +1,171 @@
+"""I3: pairwise-aggregation algebraic multigrid -- the role of AGMG.
+
+PARITY UNPINNED by the paper: AGMG's internals are not in PAPER.md (it is an
+external library).  This is the build's own, deterministic
+algorithm (DESIGN.md §2 "I3"); the CUDA path implements the
+same definition, and only this oracle pins it (plus the generic AMG sanity
+pins in tests: Galerkin identity, symmetry of the V-cycle, convergence).
+
+Definition (both sides):
+  * rows are grouped in slices (time levels); couplings across slices are never
+    used for aggregation (block-diagonal A_k: none exist; T: within-slice only).
+  * strength s_ij = |a_ij|, j != i, same slice.
+  * pairwise matching, 16 synchronous rounds: every free row i with
+    M_i = max_j s_ij (over free j) > 1e-10 |a_ii| proposes
+    p(i) = min{ j : s_ij >= (1 - tau) M_i }   (tau = 1e-8: near-ties -> lower index);
+    i and j pair iff p(i) = j and p(j) = i.  Leftovers are singletons.
+  * coarse numbering: aggregates ordered by their smallest member.
+  * two matching passes per level (pass 2 on the Galerkin matrix of pass 1),
+    so aggregates have <= 4 rows; prolongation piecewise constant; coarse
+    matrix Galerkin  A_c = P^T A P.
+  * stop: mode "A": max rows per slice <= coarse_max (64); mode "T": total rows
+    <= coarse_max (1024); or no coarsening (n_c > 0.9 n); or max_levels.
+  * smoother: damped Jacobi (omega), V(1,1) from a zero initial guess.
+  * coarsest: mode "A": per slice, grounded at the slice's first row, then the
+    slice mean removed;  mode "T": dense solve.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+TAU = 1e-8
+DECOUPLED = 1e-10
+
+
+def _row_of_nnz(A: sp.csr_matrix):
+    return np.repeat(np.arange(A.shape[0]), np.diff(A.indptr))
+
+
+def match(A: sp.csr_matrix, slice_of_row: np.ndarray, rounds: int = 16):
+    """Pairwise matching; returns (agg (n,) coarse index, nc, slice_of_coarse)."""
+    n = A.shape[0]
+    A = A.tocsr()
+    rows = _row_of_nnz(A)
+    cols = A.indices
+    s = np.abs(A.data)
+    diag = np.abs(A.diagonal())
+    coupled = (cols != rows) & (slice_of_row[cols] == slice_of_row[rows])
+    partner = np.full(n, -1, dtype=np.int64)
+    free = np.ones(n, dtype=bool)
+    for _ in range(rounds):
+        ok = coupled & free[rows] & free[cols]
+        sv = np.where(ok, s, -np.inf)
+        Mrow = np.full(n, -np.inf)
+        np.maximum.at(Mrow, rows, sv)
+        has = free & (Mrow > DECOUPLED * diag)
+        cand = ok & has[rows] & (s >= (1.0 - TAU) * Mrow[rows])
+        prop = np.full(n, np.iinfo(np.int64).max, dtype=np.int64)
+        np.minimum.at(prop, rows[cand], cols[cand])
+        prop[~has] = -1
+        i = np.nonzero(prop >= 0)[0]
+        mutual = i[prop[prop[i]] == i]
+        partner[mutual] = prop[mutual]
+        free[mutual] = False
+    leader = np.where(partner >= 0, np.minimum(np.arange(n), partner), np.arange(n))
+    is_leader = leader == np.arange(n)
+    cidx = np.cumsum(is_leader) - 1
+    agg = cidx[leader]
+    nc = int(is_leader.sum())
+    return agg, nc, slice_of_row[is_leader]
+
+
+def galerkin(A: sp.csr_matrix, agg: np.ndarray, nc: int) -> sp.csr_matrix:
+    n = A.shape[0]
+    P = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nc))
+    Ac = (P.T @ A @ P).tocsr()
+    Ac.sum_duplicates()
+    Ac.sort_indices()
+    return Ac
+
+
+@dataclass
+class Level:
+    A: sp.csr_matrix
+    slice_of_row: np.ndarray
+    dinv: np.ndarray
+    agg: np.ndarray | None = None      # fine row -> coarse row (None at the coarsest)
+    nc: int = 0
+
+
+@dataclass
+class Hierarchy:
+    levels: list
+    mode: str
+    omega: float
+    coarse_inv: list = field(default_factory=list)   # mode A: per slice (rows, inv of grounded block)
+    coarse_dense_inv: np.ndarray | None = None        # mode T
+
+    @property
+    def sizes(self):
+        return [lv.A.shape[0] for lv in self.levels]
+
+
+def _slice_sizes(slice_of_row, nslices):
+    return np.bincount(slice_of_row, minlength=nslices)
+
+
+def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
+          coarse_max: int, max_levels: int = 25) -> Hierarchy:
+    A = A.tocsr()
+    nslices = int(slice_of_row.max()) + 1 if slice_of_row.size else 0
+    levels = []
+    cur, cur_slice = A, np.asarray(slice_of_row, dtype=np.int64)
+    while True:
+        n = cur.shape[0]
+        lv = Level(A=cur, slice_of_row=cur_slice, dinv=1.0 / cur.diagonal())
+        levels.append(lv)
+        small = (_slice_sizes(cur_slice, nslices).max() <= coarse_max) if mode == "A" else (n <= coarse_max)
+        if small or len(levels) >= max_levels:
+            break
+        agg1, nc1, sl1 = match(cur, cur_slice)
+        A1 = galerkin(cur, agg1, nc1)
+        agg2, nc2, sl2 = match(A1, sl1)
+        if nc2 > 0.9 * n:
+            break
+        lv.agg = agg2[agg1]
+        lv.nc = nc2
+        cur = galerkin(A1, agg2, nc2)
+        cur_slice = sl2
+    H = Hierarchy(levels=levels, mode=mode, omega=omega)
+    Ac = levels[-1].A.toarray()
+    if mode == "A":
+        sl = levels[-1].slice_of_row
+        for k in range(nslices):
+            rows = np.nonzero(sl == k)[0]
+            blk = Ac[np.ix_(rows, rows)]
+            inv = np.linalg.inv(blk[1:, 1:]) if rows.size > 1 else np.zeros((0, 0))
+            H.coarse_inv.append((rows, inv))
+    else:
+        H.coarse_dense_inv = np.linalg.inv(Ac)
+    return H
+
+
+def _coarse_solve(H: Hierarchy, b):
+    if H.mode == "T":
+        return H.coarse_dense_inv @ b
+    x = np.zeros_like(b)
+    for rows, inv in H.coarse_inv:
+        if rows.size == 0:
+            continue
+        xs = np.zeros(rows.size)
+        xs[1:] = inv @ b[rows[1:]]          # grounded at the slice's first row
+        x[rows] = xs - xs.mean()            # then the slice mean removed
+    return x
+
+
+def vcycle(H: Hierarchy, b, level: int = 0):
+    """One V(1,1) cycle with damped Jacobi, zero initial guess."""
+    if level == len(H.levels) - 1:
+        return _coarse_solve(H, b)
+    lv = H.levels[level]
+    w = H.omega
+    x = w * lv.dinv * b                                  # pre-smooth from x = 0
+    r = b - lv.A @ x
+    bc = np.bincount(lv.agg, weights=r, minlength=lv.nc)  # restriction P^T r
+    xc = vcycle(H, bc, level + 1)
+    x = x + xc[lv.agg]                                   # prolongation
+    x = x + w * lv.dinv * (b - lv.A @ x)                 # post-smooth
+    return x

@@ -1,0 +1,121 @@
+"""I2 + a6: the BB-preconditioner (§4.5) and recovery.
+
+Projected system (4.17), P:1424-1448:
+    J_P = [[A, B^T P^T], [P B, -P C P^T]],  rhs (f; P g̃).
+Ideal block-triangular preconditioner (4.18)-(4.20), with the Schur
+complement replaced through the approximate commutation (4.22), and
+solved as (4.26).  BB apply on (r1; r2):
+  (i)   T z = -r2  by GMRES(10) + one AMG(T) V-cycle, relative eps_T (1e-1)
+  (ii)  y = P^T (M̄^{-1} Ã z)
+  (iii) b = r1 - B^T P^T y;  b^k -= mean(b^k)            (compatibility)
+  (iv)  A_k x^k = b^k by PCG + AMG(A_k) V-cycle, relative eps_A (A14: 1e-3), x^k -= mean
+Recovery (a6): δρ := P^T y (A30); δφ̃^k -= c^T δφ̃^k/|Ω| (A11);
+  δλ = Ē(g̃ - B δφ̃ + C δρ)/|Ω|;
+  δφ^k = δφ̃^k + Σ_{i=1}^{k-1} Δt δλ^i  (4.15 with A10);  δs = ρ^{-1}(h - s δρ).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import amg
+from .krylov import fgmres, pcg_slices
+from .ops import Discretisation
+
+
+@dataclass
+class SolverOpts:
+    eps_out: float = 1e-10        # A16
+    eps_T: float = 1e-1
+    eps_A: float = 1e-3           # A14 (paper: 5e-2 with AGMG)
+    restart: int = 30             # A15
+    maxit: int = 400
+    restart_T: int = 10
+    maxit_inner: int = 50
+    omega_A: float = 2.0 / 3.0
+    omega_T: float = 0.7
+    coarse_max_A: int = 64        # rows per slice
+    coarse_max_T: int = 1024      # rows in total
+    exact_inner: bool = False     # pin mode: exact T solve + exact A_k^+ (no AMG)
+
+
+class BBSolver:
+    """Per-Newton-step setup (a1, a3) + solve (a2, a4, a5) + recovery (a6)."""
+
+    def __init__(self, disc: Discretisation, phi, rho, s, mu, opts: SolverOpts | None = None):
+        self.d = d = disc
+        self.o = o = opts or SolverOpts()
+        self.phi, self.rho, self.s, self.mu = (np.asarray(phi, float), np.asarray(rho, float),
+                                               np.asarray(s, float), float(mu))
+        # a1: residuals / right-hand sides
+        self.f, self.g, self.h, self.gt = d.newton_rhs(phi, rho, s, mu)
+        self.scale = float(np.sqrt(self.f @ self.f + self.g @ self.g + self.h @ self.h))
+        self.rhs = np.concatenate([self.f, d.P(self.gt)])
+        # a2 operators
+        self.JP, self.A, self.B, self.BT, self.C = d.make_JP(phi, rho, s)
+        # a3: BB setup
+        self.Atilde = d.Atilde(rho)
+        self.T = d.T_matrix(phi, rho, s)
+        self.Mbar_t = np.tile(d.Mbar, d.K)
+        self.inner_T_its = 0
+        self.inner_A_its = []
+        if o.exact_inner:
+            self.Tinv = np.linalg.inv(self.T.toarray())
+            self.Apinv = [np.linalg.pinv(Ak.toarray()) for Ak in d.A_blocks(rho)]
+        else:
+            slA = np.repeat(np.arange(d.K + 1), d.N)
+            slT = np.repeat(np.arange(d.K), d.nbar)
+            self.amgA = amg.setup(self.A, slA, "A", o.omega_A, o.coarse_max_A)
+            self.amgT = amg.setup(self.T, slT, "T", o.omega_T, o.coarse_max_T)
+
+    # ---------------------------------------------------------------- a4
+    def apply(self, r):
+        d, o = self.d, self.o
+        n = d.n
+        r1, r2 = r[:n], r[n:]
+        if o.exact_inner:
+            z = self.Tinv @ (-r2)
+        else:
+            nr2 = float(np.linalg.norm(r2))
+            z, itT, _, _ = fgmres(lambda v: self.T @ v, lambda v: amg.vcycle(self.amgT, v),
+                                  -r2, nr2, o.eps_T, o.restart_T, o.maxit_inner)
+            self.inner_T_its += itT
+        y = d.PT((self.Atilde @ z) / self.Mbar_t)
+        b = (r1 - self.BT @ d.PT(y)).reshape(d.K + 1, d.N)
+        b = b - b.mean(axis=1, keepdims=True)
+        if o.exact_inner:
+            x = np.stack([self.Apinv[k] @ b[k] for k in range(d.K + 1)])
+        else:
+            x, its = pcg_slices(lambda v: self.A @ v, lambda v: amg.vcycle(self.amgA, v),
+                                b.reshape(-1), d.K + 1, o.eps_A, o.maxit_inner)
+            self.inner_A_its.append(its)
+            x = x.reshape(d.K + 1, d.N)
+        x = x - x.mean(axis=1, keepdims=True)
+        return np.concatenate([x.reshape(-1), y])
+
+    # ---------------------------------------------------------------- a5 + a6
+    def solve(self):
+        o = self.o
+        sol, its, conv, res = fgmres(self.JP, self.apply, self.rhs, self.scale,
+                                     o.eps_out, o.restart, o.maxit)
+        self.stats = dict(outer_its=its, converged=bool(conv), rel_res=res / self.scale,
+                          inner_T_its=self.inner_T_its,
+                          inner_A_its_max=int(max((a.max() for a in self.inner_A_its), default=0)),
+                          inner_A_its_total=int(sum(a.sum() for a in self.inner_A_its)))
+        self.sol = sol
+        return self.recover(sol)
+
+    def recover(self, sol):
+        d = self.d
+        K, N, n = d.K, d.N, d.n
+        dphit = sol[:n].reshape(K + 1, N).copy()
+        drho = d.PT(sol[n:])                                             # A30
+        dphit = dphit - (dphit @ d.M)[:, None] / d.area                  # A11
+        dphit = dphit.reshape(-1)
+        q = (self.gt - self.B @ dphit + self.C * drho).reshape(K, d.nbar)
+        dlam = q.sum(axis=1) / d.area
+        shift = np.concatenate([[0.0], np.cumsum(d.dt * dlam)])          # Σ_{i<k} Δt δλ^i (A10)
+        dphi = (dphit.reshape(K + 1, N) + shift[:, None]).reshape(-1)
+        ds = (self.h - self.s * drho) / self.rho
+        return dphi, drho, ds

@@ -1,0 +1,214 @@
+"""D2-D12: discrete operators, residuals, Newton blocks and BB operators.
+
+Everything is assembled literally from the paper's block formulas with
+scipy.sparse (the library primitive for sparse products); vectors are
+slice-concatenated as in P:160-173:  phi = (phi^1; ...; phi^{K+1}) (N each),
+rho, s = (rho^1; ...; rho^K) (N̄ each).  rho^0 = rho_in, rho^{K+1} = rho_f.
+
+Readings (restated in DESIGN.md §2):
+  A4  Delta t = 1/(K+1), K+1 phi slices
+  A5  time term of F_rho and B is Π^T M (not M̄ Π^T as printed P:257-260)
+  A6  F_phi has K+1 slices; F_rho, F_s have K
+  A7  C = +M̄ diag(s/rho), saddle (2,2) block = -C
+  A8  B̃ = -M Π D_t^T + G_f D_x Π H^T  (D10)
+  A9  BB Schur solve  T z = -r2,  y = P^T M̄^{-1} Ã z
+  Ã_k = +Ē_c diag(|ē| R̄ rho^k / |w̄|) Ē_c^T  (PSD; "discretizes -Delta_rho")
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from .mesh import TwoLevelMesh, build_two_level
+
+
+class Discretisation:
+    """Two-level TPFA + staggered time grid."""
+
+    def __init__(self, verts, tris, K: int, rho_in, rho_f, validate=True):
+        g: TwoLevelMesh = build_two_level(verts, tris, validate=validate)
+        self.g = g
+        self.K = int(K)
+        self.dt = 1.0 / (K + 1)                       # A4
+        self.nbar, self.N, self.NE = g.nbar, g.N, g.NE
+        self.n = self.N * (K + 1)
+        self.m = self.nbar * K
+        self.area = g.area                            # |Ω|
+        self.rho0 = np.asarray(rho_in, dtype=np.float64)
+        self.rhoK1 = np.asarray(rho_f, dtype=np.float64)
+        N, NE, nbar = g.N, g.NE, g.nbar
+        cols = np.arange(NE)
+        # E[i,k] = +1 if cell i is the left side of edge k, -1 if right
+        self.E = sp.csr_matrix((np.r_[np.ones(NE), -np.ones(NE)],
+                                (np.r_[g.e_L, g.e_R], np.r_[cols, cols])), shape=(N, NE))
+        self.grad = sp.diags(1.0 / g.w_len) @ self.E.T
+        self.div = -(self.E @ sp.diags(g.e_len))
+        # injection Π
+        self.Pi = sp.csr_matrix((np.ones(N), (np.arange(N), g.parent)), shape=(N, nbar))
+        self.M = g.c                                   # diag(|c|)
+        self.Mbar = g.cbar                             # diag(|c̄|)
+        # arithmetic reconstruction, A3 weights
+        self.Rf = sp.csr_matrix((np.r_[g.lam, 1.0 - g.lam], (np.r_[cols, cols], np.r_[g.e_L, g.e_R])),
+                                shape=(NE, N))
+        self.RE = (self.Rf @ self.Pi).tocsr()
+        we = g.w_len * g.e_len
+        self.DR = (self.RE.T @ sp.diags(we)).tocsr()
+        self.DRf = (self.Rf.T @ sp.diags(we)).tocsr()  # D3 (used by B̃, A8)
+        # coarse operators for Ã
+        cb = np.arange(g.NEbar)
+        self.Ec = sp.csr_matrix((np.r_[np.ones(g.NEbar), -np.ones(g.NEbar)],
+                                 (np.r_[g.ebar_L, g.ebar_R], np.r_[cb, cb])), shape=(nbar, g.NEbar))
+        self.Rbar = sp.csr_matrix((np.r_[g.lam_bar, 1.0 - g.lam_bar],
+                                   (np.r_[cb, cb], np.r_[g.ebar_L, g.ebar_R])), shape=(g.NEbar, nbar))
+        self.PiT_M = (self.Pi.T @ sp.diags(self.M)).tocsr()   # Π^T M  (A5)
+        self.M_Pi = (sp.diags(self.M) @ self.Pi).tocsr()      # M Π
+
+    # ------------------------------------------------------------------ slices
+    def phi_slices(self, phi):
+        return np.asarray(phi).reshape(self.K + 1, self.N)
+
+    def rho_slices(self, rho):
+        """rho^0 .. rho^{K+1} (boundary data at both ends)."""
+        r = np.asarray(rho).reshape(self.K, self.nbar)
+        return np.vstack([self.rho0[None], r, self.rhoK1[None]])
+
+    # ------------------------------------------------------------- A_k
+    def rho_tilde(self, rho):
+        """ρ̃^k = R_E((ρ^k + ρ^{k-1})/2), k = 1..K+1 -> (K+1, N_E)."""
+        R = self.rho_slices(rho)
+        return np.stack([self.RE @ (0.5 * (R[k] + R[k - 1])) for k in range(1, self.K + 2)])
+
+    def A_blocks(self, rho):
+        """A_k = -div diag(ρ̃^k) grad, k = 1..K+1."""
+        rt = self.rho_tilde(rho)
+        return [(-(self.div @ sp.diags(rt[k]) @ self.grad)).tocsr() for k in range(self.K + 1)]
+
+    def A(self, rho):
+        return sp.block_diag(self.A_blocks(rho), format="csr")
+
+    # --------------------------------------------------- residuals (2.5)-(2.7)
+    def residual(self, phi, rho, s, mu):
+        K, dt = self.K, self.dt
+        P = self.phi_slices(phi)
+        R = self.rho_slices(rho)
+        S = np.asarray(s).reshape(K, self.nbar)
+        Ak = self.A_blocks(rho)
+        F_phi = np.stack([-self.M_Pi @ ((R[k] - R[k - 1]) / dt) + Ak[k - 1] @ P[k - 1]
+                          for k in range(1, K + 2)])                      # (2.5), A6
+        gr = [self.grad @ P[k] for k in range(K + 1)]
+        F_rho = np.stack([self.PiT_M @ ((P[k] - P[k - 1]) / dt)          # A5: Π^T M
+                          + 0.25 * (self.DR @ (gr[k - 1] ** 2 + gr[k] ** 2))
+                          + self.Mbar * S[k - 1]
+                          for k in range(1, K + 1)])                      # (2.6)
+        F_s = (np.asarray(rho) * np.asarray(s) - mu)                      # (2.7)
+        return F_phi.reshape(-1), F_rho.reshape(-1), F_s
+
+    # ------------------------------------------------------ B, B^T
+    def grad_phi(self, phi):
+        P = self.phi_slices(phi)
+        return np.stack([self.grad @ P[k] for k in range(self.K + 1)])   # g^k, (K+1, N_E)
+
+    def B(self, phi):
+        """B = Π^T M D_t (A5) + H 𝒢 𝒟_x,  m x n, block bidiagonal."""
+        K, dt = self.K, self.dt
+        g = self.grad_phi(phi)
+        blocks = [[None] * (K + 1) for _ in range(K)]
+        for k in range(1, K + 1):                 # row slice k, column slices k (phi^k) and k+1
+            Gk = self.DR @ sp.diags(g[k - 1]) @ self.grad
+            Gk1 = self.DR @ sp.diags(g[k]) @ self.grad
+            blocks[k - 1][k - 1] = (-self.PiT_M / dt + 0.5 * Gk)
+            blocks[k - 1][k] = (self.PiT_M / dt + 0.5 * Gk1)
+        return sp.bmat(blocks, format="csr")
+
+    def C_diag(self, rho, s):
+        """C = M̄ diag(s/ρ)  (A7)."""
+        return np.tile(self.Mbar, self.K) * np.asarray(s) / np.asarray(rho)
+
+    # -------------------------------------------------- projector P
+    def P(self, y):
+        """(P y)^k = y^k - c̄ (1^T y^k) / |Ω|."""
+        Y = np.asarray(y).reshape(self.K, self.nbar)
+        return (Y - self.Mbar[None, :] * Y.sum(1, keepdims=True) / self.area).reshape(-1)
+
+    def PT(self, y):
+        """(P^T y)^k = y^k - 1 (c̄^T y^k) / |Ω|  (zero-mean projector)."""
+        Y = np.asarray(y).reshape(self.K, self.nbar)
+        return (Y - (Y @ self.Mbar)[:, None] / self.area).reshape(-1)
+
+    # ------------------------------------------------ Newton system (3.1)/(3.2)
+    def newton_rhs(self, phi, rho, s, mu):
+        F_phi, F_rho, F_s = self.residual(phi, rho, s, mu)
+        f, g, h = -F_phi, -F_rho, -F_s
+        gt = g - np.tile(self.Mbar, self.K) * h / np.asarray(rho)          # g̃
+        return f, g, h, gt
+
+    def jacobian(self, phi, rho, s):
+        """Full 3x3 block Jacobian (3.1) as a sparse matrix."""
+        A = self.A(rho)
+        B = self.B(phi)
+        Mb = sp.diags(np.tile(self.Mbar, self.K))
+        return sp.bmat([[A, B.T, None],
+                        [B, None, Mb],
+                        [None, sp.diags(np.asarray(s)), sp.diags(np.asarray(rho))]], format="csr")
+
+    # ------------------------------------------ projected system (4.17) matvec
+    def make_JP(self, phi, rho, s):
+        A = self.A(rho)
+        B = self.B(phi)
+        BT = B.T.tocsr()
+        C = self.C_diag(rho, s)
+        n = self.n
+
+        def JP(v):
+            x, y = v[:n], v[n:]
+            yp = self.PT(y)
+            return np.concatenate([A @ x + BT @ yp, self.P(B @ x - C * yp)])
+        return JP, A, B, BT, C
+
+    # ----------------------------------------------------- BB operators (4.22)
+    def Atilde_blocks(self, rho):
+        """Ã_k = Ē_c diag(|ē| R̄ρ^k / |w̄|) Ē_c^T, k = 1..K."""
+        g = self.g
+        R = np.asarray(rho).reshape(self.K, self.nbar)
+        out = []
+        for k in range(self.K):
+            om = g.ebar_len * (self.Rbar @ R[k]) / g.wbar_len
+            out.append((self.Ec @ sp.diags(om) @ self.Ec.T).tocsr())
+        return out
+
+    def Atilde(self, rho):
+        return sp.block_diag(self.Atilde_blocks(rho), format="csr")
+
+    def Btilde(self, phi):
+        """B̃ (n x m), D10 / A8:
+        (B̃z)^k = MΠ(z^k - z^{k-1})/Δt + ½ DR_f diag(g^k) grad Π (z^{k-1} + z^k),
+        k = 1..K+1, z^0 = z^{K+1} = 0."""
+        K, dt = self.K, self.dt
+        g = self.grad_phi(phi)
+        blocks = [[None] * K for _ in range(K + 1)]
+        for k in range(1, K + 2):                 # row slice k; column slices k-1, k of z
+            Sk = 0.5 * (self.DRf @ sp.diags(g[k - 1]) @ self.grad @ self.Pi)
+            if k <= K:
+                blocks[k - 1][k - 1] = self.M_Pi / dt + Sk
+            if k >= 2:
+                blocks[k - 1][k - 2] = -self.M_Pi / dt + Sk
+        return sp.bmat(blocks, format="csr")
+
+    def T_matrix(self, phi, rho, s):
+        """T = C M̄^{-1} Ã - B M^{-1} B̃  (4.26; C M̄^{-1} = diag(s/ρ))."""
+        At = self.Atilde(rho)
+        B = self.B(phi)
+        Bt = self.Btilde(phi)
+        Minv = sp.diags(1.0 / np.tile(self.M, self.K + 1))
+        sr = np.asarray(s) / np.asarray(rho)
+        return (sp.diags(sr) @ At - B @ (Minv @ Bt)).tocsr()
+
+    # ------------------------------------------------------ kinetic energy D12
+    def kinetic_energy(self, phi, rho):
+        """KE = Σ_{k=1}^{K+1} Δt ½ φ^k^T A_k φ^k (discrete (1.1))."""
+        P = self.phi_slices(phi)
+        Ak = self.A_blocks(rho)
+        return float(sum(self.dt * 0.5 * P[k] @ (Ak[k] @ P[k]) for k in range(self.K + 1)))
+
+    def slice_mass(self, rho):
+        return np.asarray(rho).reshape(self.K, self.nbar) @ self.Mbar

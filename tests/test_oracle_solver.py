@@ -1,0 +1,178 @@
+"""Pins for oracle I1-I6 and a6: Krylov drivers, AMG, BB preconditioner, recovery."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import amg
+from oracle.bb import BBSolver, SolverOpts
+from oracle.direct import direct_newton
+from oracle.krylov import fgmres, pcg_slices
+from oracle.ops import Discretisation
+from synthetic import initial_state, make_problem, random_state
+
+
+# ------------------------------------------------------------------ Krylov
+def test_fgmres_identity_and_exact_preconditioner():
+    """A = I -> 1 iteration; exact inverse as preconditioner -> 1 iteration."""
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(50)
+    x, its, conv, _ = fgmres(lambda v: v, lambda v: v, b, np.linalg.norm(b), 1e-12, 30, 400)
+    assert its == 1 and conv and np.allclose(x, b)
+    A = rng.standard_normal((50, 50)) + 10 * np.eye(50)
+    Ai = np.linalg.inv(A)
+    x, its, conv, _ = fgmres(lambda v: A @ v, lambda v: Ai @ v, b, np.linalg.norm(b), 1e-12, 30, 400)
+    assert its == 1 and np.allclose(A @ x, b, atol=1e-10)
+
+
+def test_fgmres_restart_and_cap():
+    """Unpreconditioned nonsymmetric system: converges with restarts; true residual
+    <= tol*scale; the cap is honoured and reported (P:1770 '400 limit')."""
+    rng = np.random.default_rng(1)
+    n = 200
+    A = sp.diags([-1.0, 2.5, -1.3], [-1, 0, 1], shape=(n, n)).tocsr()
+    b = rng.standard_normal(n)
+    x, its, conv, _ = fgmres(lambda v: A @ v, lambda v: v, b, np.linalg.norm(b), 1e-10, 10, 2000)
+    assert conv and np.linalg.norm(b - A @ x) <= 1.01e-10 * np.linalg.norm(b) * 10
+    x, its, conv, _ = fgmres(lambda v: A @ v, lambda v: v, b, np.linalg.norm(b), 1e-14, 5, 7)
+    assert its == 7 and not conv
+
+
+def test_pcg_slices_matches_direct():
+    """Per-slice PCG on independent SPD blocks = K separate CG runs (I4)."""
+    rng = np.random.default_rng(2)
+    blocks = []
+    for k in range(3):
+        Q = rng.standard_normal((20, 20))
+        blocks.append(Q @ Q.T + (k + 1) * np.eye(20))
+    A = sp.block_diag(blocks, format="csr")
+    b = rng.standard_normal(60)
+    x, its = pcg_slices(lambda v: A @ v, lambda v: v, b, 3, 1e-12, 200)
+    assert np.allclose(x, np.linalg.solve(A.toarray(), b), rtol=1e-8)
+    assert its.shape == (3,) and np.all(its > 0)
+    # freezing: slice with b = 0 does no work
+    b2 = b.copy()
+    b2[20:40] = 0
+    x2, its2 = pcg_slices(lambda v: A @ v, lambda v: v, b2, 3, 1e-12, 200)
+    assert its2[1] == 0 and np.all(x2[20:40] == 0)
+
+
+# --------------------------------------------------------------------- AMG
+def _lap1d(n):
+    return sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(n, n)).tocsr()
+
+
+def test_matching_and_galerkin():
+    """Pairs are mutual, within a slice, aggregates <= 4 rows after 2 passes,
+    coarse = P^T A P (brute force dense)."""
+    A = sp.block_diag([_lap1d(37), _lap1d(23)], format="csr")
+    sl = np.r_[np.zeros(37, int), np.ones(23, int)]
+    agg, nc, slc = amg.match(A, sl)
+    assert np.all(np.bincount(agg) <= 2)
+    for c in range(nc):
+        mem = np.nonzero(agg == c)[0]
+        assert len(set(sl[mem])) == 1
+    H = amg.setup(A, sl, "A", 2 / 3, coarse_max=4)
+    assert np.all(np.bincount(H.levels[0].agg) <= 4)
+    P = np.zeros((60, H.levels[0].nc))
+    P[np.arange(60), H.levels[0].agg] = 1
+    assert np.allclose(H.levels[1].A.toarray(), P.T @ A.toarray() @ P, atol=1e-14)
+    # uniform weights: ties are broken towards the lower index -> (0,1),(2,3),... on level 1
+    agg1, _, _ = amg.match(_lap1d(8), np.zeros(8, int))
+    assert list(agg1) == [0, 0, 1, 1, 2, 2, 3, 3]
+
+
+def test_vcycle_symmetric_and_convergent():
+    """Mode A on a block of weighted Laplacians A_k: the V(1,1) operator is
+    symmetric on consistent vectors (CG is legitimate), and PCG reaches
+    1e-8 in few iterations."""
+    p = make_problem("C1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    _, rho, _ = random_state(p, seed=1)
+    A = d.A(rho)
+    sl = np.repeat(np.arange(d.K + 1), d.N)
+    H = amg.setup(A, sl, "A", 2 / 3, 64)
+    assert len(H.levels) >= 3 and max(np.bincount(H.levels[-1].slice_of_row)) <= 64
+    rng = np.random.default_rng(3)
+
+    def consistent(v):
+        V = v.reshape(d.K + 1, d.N)
+        return (V - V.mean(1, keepdims=True)).reshape(-1)
+    u, v = consistent(rng.standard_normal(d.n)), consistent(rng.standard_normal(d.n))
+    Mu, Mv = consistent(amg.vcycle(H, u)), consistent(amg.vcycle(H, v))
+    assert abs(Mu @ v - u @ Mv) < 1e-10 * abs(Mu @ v)
+    x, its = pcg_slices(lambda q: A @ q, lambda q: amg.vcycle(H, q), u, d.K + 1, 1e-8, 100)
+    assert its.max() < 60
+    r = (u - A @ x).reshape(d.K + 1, d.N)
+    assert np.all(np.linalg.norm(r, axis=1) <= 1e-8 * np.linalg.norm(u.reshape(d.K + 1, d.N), axis=1))
+    # coarsening: >= 2.5x per level on the fine levels (two pairwise passes)
+    sz = H.sizes
+    assert sz[0] / sz[1] > 2.5 and sz[1] / sz[2] > 2.5
+
+
+# ----------------------------------------------------------- BB / recovery
+def test_ideal_preconditioner_two_iterations():
+    """(4.18) with the exact projected Schur complement S = -P(C + B A^+ B^T)P^T
+    and exact A^+ makes FGMRES converge in 2 iterations."""
+    p = make_problem("T0")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=2, mu=0.1)
+    S0 = BBSolver(d, phi, rho, s, 0.1, SolverOpts(exact_inner=True))
+    A = S0.A.toarray()
+    Ap = np.linalg.pinv(A)
+    B = S0.B.toarray()
+    Pm = np.stack([d.P(e) for e in np.eye(d.m)], 1)
+    S = -Pm @ (np.diag(S0.C) + B @ Ap @ B.T) @ Pm.T
+    Sp = np.linalg.pinv(S)
+    n = d.n
+
+    def U_inv(r):
+        y = Pm.T @ (Sp @ r[n:])
+        x = Ap @ (r[:n] - B.T @ (Pm.T @ y))
+        return np.concatenate([x, y])
+    _, its, conv, _ = fgmres(S0.JP, U_inv, S0.rhs, S0.scale, 1e-10, 30, 400)
+    assert conv and its == 2
+
+
+@pytest.mark.parametrize("name,exact", [("T1", True), ("T1", False), ("T2b", False)])
+def test_bb_solve_matches_direct(name, exact):
+    """BB-FGMRES (4.17) + recovery (a6) reproduces the dense direct solution of
+    (3.1) (north star: Krylov vs dense direct on tiny instances)."""
+    p = make_problem(name)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=7, mu=0.05)
+    dphi0, drho0, ds0, J, rhs = direct_newton(d, phi, rho, s, 0.05)
+    # restart 100: the T2b random state (vanishing rho_in) stagnates FGMRES(30)
+    S = BBSolver(d, phi, rho, s, 0.05, SolverOpts(exact_inner=exact, eps_out=1e-12, restart=100))
+    dphi, drho, ds = S.solve()
+    assert S.stats["converged"]
+    for a, b in ((dphi, dphi0), (drho, drho0), (ds, ds0)):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b)
+    # the recovered direction satisfies (3.1) (A10, A30)
+    res = J @ np.concatenate([dphi, drho, ds]) - rhs
+    assert np.linalg.norm(res) <= 1e-9 * np.linalg.norm(rhs)
+
+
+def test_recovery_residual_equals_projected_residual():
+    """A16: after recovery, ||res(3.2)|| = ||res(4.17)|| for an approximate solution."""
+    p = make_problem("T1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=8, mu=0.05)
+    S = BBSolver(d, phi, rho, s, 0.05, SolverOpts(exact_inner=True, eps_out=1e-3))
+    dphi, drho, ds = S.solve()
+    r417 = S.JP(S.sol) - S.rhs
+    J32 = sp.bmat([[S.A, S.B.T], [S.B, -sp.diags(S.C)]]).tocsr()
+    r32 = J32 @ np.concatenate([dphi, drho]) - np.concatenate([S.f, S.gt])
+    assert abs(np.linalg.norm(r32) / np.linalg.norm(r417) - 1) < 1e-6
+
+
+@pytest.mark.parametrize("L,K,table", [(1, 4, 6), (2, 8, 8)])
+def test_bb_counts_vs_table4(L, K, table):
+    """Outer FGMRES iterations at mu = 1 with exact inner solves within a factor 2
+    of Table 4's first row (6 and 8 at eps_out = 1e-5), test case 2
+    (translated compact bump).  S:605 acceptance band."""
+    p = make_problem("T2b", L=L, K=K)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    S = BBSolver(d, phi, rho, s, 1.0, SolverOpts(exact_inner=True, eps_out=1e-5))
+    S.solve()
+    assert table / 2 <= S.stats["outer_its"] <= 2 * table
