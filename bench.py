@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py -- Newton-system solves/s of the BB-preconditioned IPM solver on B200.
+
+One *step* = one pass of the whole hot path on one Newton
+system: restore the state (device copy), assemble (residual/RHS, edge weights,
+C, T, AMG(A), AMG(T) setup), FGMRES on (4.17) with the BB preconditioner,
+recovery of (dphi, drho, ds), step length + update + renormalisation.
+
+Workload (default): BASELINE.json configs[1] = C2 (64x64-grid-sized acute mesh,
+8192 triangles, Nt = K = 32, seeded jitter), the first Newton system of the IPM
+(A19 initial point, mu = 1), eps_out = 1e-10.  Inputs are synthetic
+(synthetic/), fp64 throughout.
+
+    python bench.py [--gpus N --steps K --warmup W --config C2 --impl bbot|reference]
+
+N > 1 (torchrun): every rank solves its own replica of the workload (weak
+scaling, no data-path collective; time-slab sharding is not built yet -- see
+DESIGN.md §6).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+COUNTS_FILE = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bbot", choices=["bbot", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--profile-out", default=None, help="write the per-kernel table (json) here")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_FILE))["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def byte_models(ctx, nnzT):
+    """Algorithmic (compulsory) bytes per launch of the main kernels."""
+    n, m, N, NE, K, nbar = ctx.n, ctx.m, ctx.N, ctx.NE, ctx.K, ctx.nbar
+    W = ctx.T_width
+    A_sizes, T_sizes = ctx.amg_info(0), ctx.amg_info(1)
+    nc1A = A_sizes[1] if len(A_sizes) > 1 else 0
+    nc1T = T_sizes[1] if len(T_sizes) > 1 else 0
+    om = 8 * (K + 1) * NE + 32 * N          # edge weights + cell->edge tables (once)
+    tT = 8 * nnzT + 4 * W * nbar            # T values + shared column pattern
+    return {
+        "void bbot::k_spmv<bbot::EdgeLapView>": 16 * n + om,
+        "void bbot::k_down<bbot::EdgeLapView>": 32 * n + om,
+        "void bbot::k_up<bbot::EdgeLapView>": 36 * n + 8 * nc1A + om,
+        "void bbot::k_spmv<bbot::SliceEllView>": tT + 16 * m,
+        "void bbot::k_down<bbot::SliceEllView>": tT + 32 * m,
+        "void bbot::k_up<bbot::SliceEllView>": tT + 36 * m + 8 * nc1T,
+        "bbot::k_pcg_xr(long long, int, double const*, double*, double*, double const*, double const*)": 48 * n,
+        "bbot::k_pcg_p(long long, int, double const*, double const*, double*)": 24 * n,
+    }
+
+
+def oracle_sample(config, n_outer_sample=3):
+    """Bounded oracle sample on this host: assembly + AMG setups + n_outer_sample
+    FGMRES iterations of the same Newton system, single core.  Returns
+    (seconds_setup, seconds_per_outer)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.bb import BBSolver, SolverOpts
+    from oracle.ops import Discretisation
+    from synthetic import initial_state, make_problem
+    p = make_problem(config)
+    phi, rho, s = initial_state(p, 1.0)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+        S = BBSolver(d, phi, rho, s, 1.0, SolverOpts(maxit=n_outer_sample))
+        t1 = time.perf_counter()
+        S.solve()
+        t2 = time.perf_counter()
+    return t1 - t0, (t2 - t1) / max(1, S.stats["outer_its"])
+
+
+def oracle_outer_count(config):
+    try:
+        return int(json.load(open(COUNTS_FILE))[f"{config}/init/mu=1"]["outer_its"])
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_outer = oracle_outer_count(args.config)
+    if n_outer is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"no oracle outer count for {args.config}"}))
+        return
+    for _ in range(args.warmup):
+        oracle_sample(args.config)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        ts, to = oracle_sample(args.config)
+        t_solve = ts + n_outer * to
+        vals.append(1.0 / t_solve)
+        t_all += t_solve
+    value = args.steps / t_all
+    sample = (f"per step: oracle assembly + AMG setups + 3 FGMRES iterations of the {args.config} mu=1 system, "
+              f"1 core, extrapolated to the oracle's own {n_outer} outer iterations")
+    line = {"impl": "reference", "metric": "newton_solves_per_s", "value": value, "unit": "solves/s",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} first IPM Newton system (mu=1), eps_out=1e-10"},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if (args.impl == "bbot" and torch.cuda.is_available()) else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    import numpy as np
+
+    import paper_2209_00315_b200 as pb
+    from synthetic import initial_state, make_problem
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    p = make_problem(args.config)
+    phi_h, rho_h, s_h = initial_state(p, 1.0)
+    mu = 1.0
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream)
+    phi_d = torch.tensor(phi_h, device=dev)
+    rho_d = torch.tensor(rho_h, device=dev)
+    s_d = torch.tensor(s_h, device=dev)
+    last = {}
+
+    def step():
+        ctx.set_state(phi_d, rho_d, s_d, mu)            # device -> device restore of the input state
+        ctx.assemble()                                   # a1 + a3
+        last["st"] = ctx.solve_stats_only()              # a2 + a4 + a5 + a6 (direction stays in HBM)
+        last["alpha"] = ctx.newton_update(0.95)          # a7
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    clocks = clk.stop()
+    t = e0.elapsed_time(e1) / 1e3
+    launches = (ctx.launch_count() - l0) // args.steps
+    if dist is not None:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    value = world * args.steps / t
+    st = last["st"]
+
+    # ---- end to end through the C-ABI with host buffers (H2D of the state, D2H of the new state)
+    phi_o, rho_o, s_o = np.empty_like(phi_h), np.empty_like(rho_h), np.empty_like(s_h)
+
+    def step_e2e():
+        ctx.set_state(phi_h, rho_h, s_h, mu)
+        ctx.assemble()
+        ctx.solve_stats_only()
+        ctx.newton_update(0.95)
+        ctx.get_state(phi_o, rho_o, s_o)
+
+    step_e2e()
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = e0.elapsed_time(e1) / 1e3
+    if dist is not None:
+        tt = torch.tensor([te], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    io_bytes = 8 * (ctx.n + 2 * ctx.m)
+
+    # ---- per-kernel shares (one extra profiled step, CUDA events around every launch)
+    roof = None
+    prof_table = None
+    if not args.no_profile:
+        ctx.prof_start()
+        step()
+        prof_table = ctx.prof_stop()
+        nnzT, _ = ctx.T_nnz()
+        models = byte_models(ctx, nnzT)
+        total_ms = sum(v[1] for v in prof_table.values())
+        ranked = sorted(prof_table.items(), key=lambda kv: -kv[1][1])
+        dom = next(((k, v) for k, v in ranked if k in models), None)
+        peak, peak_kind = hbm_peak()
+        if dom is not None:
+            name, (cnt, ms) = dom
+            avg_s = ms / cnt / 1e3
+            ach = models[name] / avg_s / 1e9
+            traffic = None
+            try:
+                summ = json.load(open(NCU_SUMMARY))
+                traffic = summ.get("dram_bytes_per_launch", {}).get(name)
+            except Exception:
+                pass
+            roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": models[name], "avg_launch_us": round(avg_s * 1e6, 2),
+                    "share_of_step": round(ms / total_ms, 4), "top_kernel": ranked[0][0],
+                    "top_kernel_share": round(ranked[0][1][1] / total_ms, 4)}
+        if args.profile_out and rank == 0:
+            json.dump({"config": args.config, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in ranked},
+                       "total_ms": total_ms, "models": models}, open(args.profile_out, "w"), indent=1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_outer = oracle_outer_count(args.config)
+        if n_outer is not None:
+            ts, to = oracle_sample(args.config)
+            cpu = {"value": 1.0 / (ts + n_outer * to), "unit": "solves/s", "cores": 1, "kind": "oracle",
+                   "sample": (f"oracle assembly + AMG setups + 3 FGMRES iterations of the same {args.config} mu=1 "
+                              f"system on 1 host core ({ts:.1f} s setup, {to:.2f} s/outer), extrapolated to the "
+                              f"oracle's own {n_outer} outer iterations (tests/golden/oracle_counts.json)")}
+
+    if rank == 0:
+        line = {
+            "metric": "newton_solves_per_s", "value": value, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: first IPM Newton system (A19 point, mu=1), eps_out=1e-10",
+                       "nbar": ctx.nbar, "K": ctx.K, "n_plus_m": ctx.n + ctx.m,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "no flush; per-step working set (FGMRES basis 61 x (n+m) x 8 B) exceeds the 126 MB L2"},
+            "unknowns_per_s": value * (ctx.n + ctx.m),
+            "solve": {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "converged", "rel_res",
+                                         "amg_levels_A", "amg_levels_T")},
+            "e2e": {"value": world * args.steps / te, "unit": "solves/s", "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/* bbot.h -- C-ABI of libbbot.so, the B200-native (sm_100a, fp64) hot path of
+ * arXiv 2209.00315: the BB-preconditioned Krylov solve of the interior-point
+ * Newton saddle-point system of the two-level TPFA finite-volume discretisation
+ * of the Benamou-Brenier optimal-transport problem, plus the per-Newton-step
+ * assembly, recovery and the IPM loop that feed it.
+ *
+ * Citation keys: P:n = /root/reference/PAPER.md line n (LaTeX source of the
+ * paper).  Equation numbers follow the LaTeX labels; readings A1-A30 of the
+ * paper's ambiguities are listed in DESIGN.md §2.
+ *
+ * Conventions (all calls):
+ *  - Sizes: Nbar coarse triangles, N = 3 Nbar fine kites, K interior density
+ *    levels, Delta t = 1/(K+1), n = N (K+1) potential unknowns,
+ *    m = Nbar K density unknowns.
+ *  - Vectors are slice-major fp64: phi = (phi^1;...;phi^{K+1}), slice k holds
+ *    N values, fine kite 3t+s = kite at local vertex s of triangle t;
+ *    rho = (rho^1;...;rho^K), s likewise, Nbar values per slice.
+ *  - bbot_mem tells whether a vector pointer is HOST memory or DEVICE memory on
+ *    the context's device.  Host pointers are copied synchronously inside the
+ *    call; device pointers must stay valid until the call returns and are used
+ *    on the context's stream.  The caller owns every buffer it passes; the
+ *    library owns its device workspace (cudaMallocAsync on the ctx stream).
+ *  - Every call returns a bbot_status; bbot_last_error() holds a message.
+ *    Non-convergence (FGMRES cap, "the 400 limit") is recorded in the
+ *    stats (converged = 0) and returns BBOT_OK: the best iterate is kept.
+ *  - Calls on one context are serialised; a context is not thread-safe.
+ *  - There is no CPU fallback: every arithmetic step runs in CUDA kernels.
+ */
+#ifndef BBOT_H
+#define BBOT_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bbot_ctx bbot_ctx;
+
+typedef enum {
+  BBOT_OK = 0,
+  BBOT_E_INPUT = 1,     /* bad argument (NULL, size, K < 1, option out of range)        */
+  BBOT_E_GEOMETRY = 2,  /* mesh not acute / not CCW / not TPFA-admissible      */
+  BBOT_E_STATE = 3,     /* rho <= 0 or s <= 0 in a state (IPM interior)           */
+  BBOT_E_NOCONV = 4,    /* reserved (non-convergence is reported in stats, not here)     */
+  BBOT_E_CUDA = 5,      /* CUDA runtime error (message has the CUDA string)              */
+  BBOT_E_NOMEM = 7,     /* device allocation failed                                     */
+  BBOT_E_INTERNAL = 8,  /* internal capacity exceeded (AMG row too wide) / bug           */
+  BBOT_E_ORDER = 9      /* call order (e.g. solve before assemble)                      */
+} bbot_status;
+
+typedef enum { BBOT_MEM_HOST = 0, BBOT_MEM_DEVICE = 1 } bbot_mem;
+
+/* Solver options (A14-A16, I3).  Defaults in brackets. */
+typedef struct {
+  double eps_out;      /* outer FGMRES tol on ||res(4.17)|| / ||(f;g;h)|| [1e-10] (A16) */
+  double eps_T;        /* inner GMRES tol for T z = -r2, relative [1e-1]           */
+  double eps_A;        /* inner PCG tol for A_k x = b, relative [1e-3] (A14; paper 5e-2)    */
+  int restart;         /* FGMRES restart [30] (A15)                                         */
+  int maxit;           /* FGMRES cap [400]                                         */
+  int restart_T;       /* inner GMRES restart [10]                                          */
+  int maxit_inner;     /* inner caps (T GMRES total its, per-slice PCG its) [50]            */
+  double omega_A;      /* damped-Jacobi weight, AMG(A) [2/3]                                */
+  double omega_T;      /* damped-Jacobi weight, AMG(T) [0.7]                                */
+  int coarse_max_A;    /* AMG(A) coarsest: max rows per time slice [64]                     */
+  int coarse_max_T;    /* AMG(T) coarsest: max rows in total [1024]                         */
+} bbot_solver_opts;
+
+typedef struct {
+  int outer_its;            /* FGMRES iterations (P:601 Outer/Lin.sys)                     */
+  int inner_T_its;          /* total T-GMRES iterations (P:607 Inner/Outer numerator)      */
+  int inner_A_its_max;      /* max per-slice PCG iterations in any apply                   */
+  long long inner_A_its_total;
+  int converged;            /* 1 if ||res|| <= eps_out ||(f;g;h)||                          */
+  double rel_res;           /* final Arnoldi residual / ||(f;g;h)||                         */
+  double scale;             /* ||(f;g;h)||                                                  */
+  double t_assemble_ms;     /* a1 + T assembly                                              */
+  double t_setup_ms;        /* AMG(A) + AMG(T) setup (the paper's "% preprocess")   */
+  double t_krylov_ms;       /* FGMRES incl. BB applies                                      */
+  double t_recover_ms;      /* a6                                                           */
+  int amg_levels_A, amg_levels_T;
+} bbot_solve_stats;
+
+typedef struct {
+  double mu0;               /* [1]     (A17)                                                */
+  double mu_factor;         /* [0.5]   (A17)                                                */
+  double mu_min;            /* [1e-8]  (A17: last mu = 2^-26)                                */
+  double newton_rel_tol;    /* [1e-2]  stop ||F|| <= max(tol*mu, floor)*||F(x0;mu0)|| (A18)  */
+  double newton_abs_floor;  /* [1e-11]                                                      */
+  double frac_to_boundary;  /* [0.95]  (A20)                                                */
+  int newton_max;           /* [30]    Newton steps per mu (A18)                             */
+  int max_mu_steps;         /* [0 = all] truncate the mu schedule                           */
+} bbot_ipm_opts;
+
+typedef struct {
+  double mu; int newton; double alpha; double res_norm;
+  bbot_solve_stats solve;
+} bbot_ipm_record;
+
+typedef void (*bbot_ipm_cb)(const bbot_ipm_record* rec, void* user);
+
+typedef struct {
+  int n_systems;            /* Newton systems solved                                        */
+  long long total_outer;    /* sum of outer iterations                                      */
+  long long total_inner_T;
+  int n_unconverged;        /* systems that hit the FGMRES cap (the paper's dagger)         */
+  double final_mu;
+  double kinetic_energy;    /* D12 at the final state                                       */
+  double wall_ms;
+} bbot_ipm_stats;
+
+void bbot_default_solver_opts(bbot_solver_opts* o);
+void bbot_default_ipm_opts(bbot_ipm_opts* o);
+
+/* Create a context on the current CUDA device.
+ * vertices: host, nv x 2 (x,y); tris: host, nt x 3 vertex indices, CCW.
+ * rho_in / rho_f: host, nt coarse cell averages, >= 0, equal mass.
+ * Builds the coarse + fine TPFA geometry on the host (readings A2, A3),
+ * validates it (acute, CCW, orthogonal, |w| > 0) -> BBOT_E_GEOMETRY, and
+ * uploads it.  opts may be NULL (defaults).  stream: a cudaStream_t or NULL
+ * (the legacy default stream).  The state is set to the A19 initial point
+ * at mu = 1. */
+bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt, int K,
+                        const double* rho_in, const double* rho_f,
+                        const bbot_solver_opts* opts, void* stream, bbot_ctx** out);
+void bbot_destroy(bbot_ctx* ctx);
+const char* bbot_last_error(const bbot_ctx* ctx);
+
+bbot_status bbot_sizes(const bbot_ctx* ctx, long long* nbar, long long* N, long long* NE,
+                       int* K, long long* n, long long* m);
+bbot_status bbot_set_opts(bbot_ctx* ctx, const bbot_solver_opts* opts);
+/* T storage: spatial stencil width W (slots per slice offset) and structural nnz. */
+bbot_status bbot_T_info(const bbot_ctx* ctx, int* W, long long* nnz);
+
+/* State (phi n, rho m, s m) and the barrier parameter mu.  set_state checks
+ * rho > 0 and s > 0 (BBOT_E_STATE) and invalidates the assembly. */
+bbot_status bbot_set_state(bbot_ctx* ctx, const double* phi, const double* rho,
+                           const double* s, double mu, bbot_mem mem);
+bbot_status bbot_get_state(bbot_ctx* ctx, double* phi, double* rho, double* s,
+                           double* mu, bbot_mem mem);
+/* A19 initial point: rho^k uniform with the boundary mass, s = mu0/rho, phi = 0. */
+bbot_status bbot_init_state(bbot_ctx* ctx, double mu0);
+
+/* Residuals (2.5)-(2.7) (A5, A6) at the current state; any output may be
+ * NULL.  norm = ||(F_phi;F_rho;F_s)||_2. */
+bbot_status bbot_residual(bbot_ctx* ctx, double* F_phi, double* F_rho, double* F_s,
+                          double* norm, bbot_mem mem);
+
+/* a1 + a3: per-Newton-step assembly at the current state: edge weights, grad phi,
+ * C = Mbar diag(s/rho) (A7), RHS (f; P g~) ((4.17)), Atilde,
+ * T = C Mbar^-1 Atilde - B M^-1 Btilde ((4.26), A8) and both AMG hierarchies. */
+bbot_status bbot_assemble(bbot_ctx* ctx);
+
+/* a2: y = J_P x with J_P = [[A, B^T P^T],[P B, -P C P^T]] ((4.17)).
+ * x, y: n+m vectors. Requires bbot_assemble. */
+bbot_status bbot_jp_matvec(bbot_ctx* ctx, const double* x, double* y, bbot_mem mem);
+
+/* a4: z = BB-preconditioner applied to r (n+m): T z2 = -r2 (GMRES+AMG(T)),
+ * y = P^T Mbar^-1 Atilde z2, b = r1 - B^T P^T y (slice means removed),
+ * A_k x^k = b^k (PCG+AMG(A)), out (x; y)  ((4.18)-(4.20), (4.26), A9, A12, A14). */
+bbot_status bbot_bb_apply(bbot_ctx* ctx, const double* r, double* z, bbot_mem mem,
+                          int* inner_T_its, int* inner_A_its_max);
+
+/* a5 + a6: FGMRES on (4.17) with the BB preconditioner, then recovery of
+ * (dphi, drho, ds) ((4.15) with A10, A30).  Outputs may be
+ * NULL (the direction is always kept in the context for bbot_newton_update). */
+bbot_status bbot_solve(bbot_ctx* ctx, double* dphi, double* drho, double* ds,
+                       bbot_solve_stats* st, bbot_mem mem);
+
+/* a7: step length (fraction to boundary, A20), update of (phi, rho, s) with the
+ * last direction, per-slice renormalisation of rho (Remark 3.2). */
+bbot_status bbot_newton_update(bbot_ctx* ctx, double frac_to_boundary, double* alpha);
+
+/* a7: full IPM run from the current state (mu schedule A17, Newton stop A18). */
+bbot_status bbot_ipm_run(bbot_ctx* ctx, const bbot_ipm_opts* o, bbot_ipm_stats* st,
+                         bbot_ipm_cb cb, void* user);
+
+/* D12: KE = sum_k Delta t 1/2 phi^k^T A_k phi^k at the current state. */
+bbot_status bbot_kinetic_energy(bbot_ctx* ctx, double* ke);
+
+/* ---- inspection (parity tests, profiling) ---- */
+/* T as host CSR (rows m; columns sorted).  Call with rowptr == NULL to get nnz. */
+bbot_status bbot_get_T(bbot_ctx* ctx, long long* nnz, long long* rowptr, int* cols, double* vals);
+/* which: 0 = AMG(A), 1 = AMG(T).  sizes: >= 32 entries. */
+bbot_status bbot_amg_info(bbot_ctx* ctx, int which, int* nlevels, long long* sizes);
+/* fine-row -> coarse-row map of level `level` (host, length sizes[level]). */
+bbot_status bbot_amg_agg(bbot_ctx* ctx, int which, int level, int* agg);
+/* one V-cycle x = M^-1 b on level 0 of hierarchy `which` (length n or m). */
+bbot_status bbot_amg_vcycle(bbot_ctx* ctx, int which, const double* b, double* x, bbot_mem mem);
+/* count of CUDA kernel launches issued by this context since creation. */
+long long bbot_launch_count(const bbot_ctx* ctx);
+/* Per-launch profiler: between start and stop every kernel launch is bracketed
+ * by CUDA events on the context stream (adds ~2 event records per launch; use
+ * for kernel shares, not for the headline timing).  stop writes a text table
+ * "demangled-name<TAB>launches<TAB>total_ms" into buf (NUL-terminated,
+ * truncated to buflen) and the required size into *needed. */
+bbot_status bbot_prof_start(bbot_ctx* ctx);
+bbot_status bbot_prof_stop(bbot_ctx* ctx, char* buf, long long buflen, long long* needed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BBOT_H */

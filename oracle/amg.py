@@ -9,7 +9,8 @@ pins in tests: Galerkin identity, symmetry of the V-cycle, convergence).
 Definition (both sides):
   * rows are grouped in slices (time levels); couplings across slices are never
     used for aggregation (block-diagonal A_k: none exist; T: within-slice only).
-  * strength s_ij = |a_ij|, j != i, same slice.
+  * strength s_ij = (|a_ij| + |a_ji|)/2, j != i, same slice (symmetrised so that
+    mutual-maximum matching always progresses on nonsymmetric T).
   * pairwise matching, 16 synchronous rounds: every free row i with
     M_i = max_j s_ij (over free j) > 1e-10 |a_ii| proposes
     p(i) = min{ j : s_ij >= (1 - tau) M_i }   (tau = 1e-8: near-ties -> lower index);
@@ -43,11 +44,17 @@ def match(A: sp.csr_matrix, slice_of_row: np.ndarray, rounds: int = 16):
     """Pairwise matching; returns (agg (n,) coarse index, nc, slice_of_coarse)."""
     n = A.shape[0]
     A = A.tocsr()
-    rows = _row_of_nnz(A)
-    cols = A.indices
-    s = np.abs(A.data)
     diag = np.abs(A.diagonal())
-    coupled = (cols != rows) & (slice_of_row[cols] == slice_of_row[rows])
+    # symmetrised within-slice strength S = (|A| + |A|^T)/2 restricted to i != j, same slice
+    rows = _row_of_nnz(A)
+    keep = (A.indices != rows) & (slice_of_row[A.indices] == slice_of_row[rows])
+    S = sp.csr_matrix((np.abs(A.data[keep]), (rows[keep], A.indices[keep])), shape=A.shape)
+    S = ((S + S.T) * 0.5).tocsr()
+    S.sort_indices()
+    rows = _row_of_nnz(S)
+    cols = S.indices
+    s = S.data
+    coupled = np.ones(cols.size, dtype=bool)
     partner = np.full(n, -1, dtype=np.int64)
     free = np.ones(n, dtype=bool)
     for _ in range(rounds):

@@ -1,0 +1,97 @@
+// ctx.cuh -- the opaque bbot_ctx: device-resident geometry, state, per-Newton-
+// step assembly, AMG hierarchies and Krylov workspaces.
+//
+// HBM layout: everything slice-major fp64.
+//   phi      [K+1][N]          rho_ext [K+2][Nbar] (slices 0 and K+1 = rho_in, rho_f)
+//   s        [K][Nbar]         omega, gphi [K+1][N_E]   (edge weights, grad phi)
+//   omegabar [K][Nbar_E]       T values [K][3][W][Nbar] (slot-major ELL, pattern shared
+//                                                        by all slices: tcol [W][Nbar])
+#pragma once
+#include "common.cuh"
+#include "geometry.h"
+#include "amg.cuh"
+#include "krylov.cuh"
+#include <string>
+#include <memory>
+
+namespace bbot {
+
+// Per-coarse-cell tables for B rows and T assembly (built on the host, tassemble.cu).
+constexpr int CE_MAX = 9;    // fine edges sigma with R_E[sigma,i] != 0 (3 type a + <= 6 type b)
+constexpr int FI_MAX = 9;    // fine cells in a B row (3 children + <= 6 across i's boundary)
+constexpr int FI_EMAX = 4;   // edges of E(i) incident to such a fine cell
+constexpr int TB_MAX = 2;    // type-b edges of a fine cell
+constexpr int W_MAX = 16;    // T spatial stencil width cap
+
+struct DevGeom {
+  int nbar = 0, N = 0, NE = 0, NEbar = 0, K = 0, W = 0;
+  long long Tnnz = 0;                         // structural nnz of T
+  double dt = 0, area = 0;
+  DBuf<double> cbar, c;                       // areas
+  DBuf<int> ebL, ebR;                         // coarse internal edges
+  DBuf<double> ebar_coef, lam_bar;            // |e-bar|/|w-bar|, lambda-bar
+  DBuf<int> cadj_e, cadj_nb;                  // [3][nbar]
+  DBuf<int> eL, eR;                           // fine internal edges
+  DBuf<double> e_len, w_len, lam;
+  DBuf<int> fadj_e, fadj_nb;                  // [4][N]
+  // B-row edge list per coarse cell: (edge, R_E[sigma,i])
+  DBuf<int> ce_edge;                          // [CE_MAX][nbar], -1 pad
+  DBuf<double> ce_coef;                       // [CE_MAX][nbar]
+  // T assembly tables
+  DBuf<int> tcol;                             // [W][nbar] spatial columns, -1 pad; tcol[0][i] = i
+  DBuf<int> fi_cell;                          // [FI_MAX][nbar] fine cell, -1 pad
+  DBuf<int> fi_child;                         // [FI_MAX][nbar] 1 if child of i
+  DBuf<int> fi_ppos;                          // [FI_MAX][nbar] pos of par(f) in S(i)
+  DBuf<int> fi_edge;                          // [FI_MAX][FI_EMAX][nbar]
+  DBuf<double> fi_alpha;                      // [FI_MAX][FI_EMAX][nbar] 1/2 R_E|e| E[f,sigma]
+  DBuf<int> fi_tbe;                           // [FI_MAX][TB_MAX][nbar] type-b edges of f
+  DBuf<double> fi_tbbeta;                     // [FI_MAX][TB_MAX][nbar] 1/2 R_f[sigma,f]|e|
+  DBuf<int> fi_tbpL, fi_tbpR;                 // [FI_MAX][TB_MAX][nbar] pos of par L/R in S(i)
+  DBuf<int> ca_pos;                           // [3][nbar] pos of coarse neighbour in S(i)
+  DBuf<int> slice_A, slice_T;                 // row -> slice for AMG level 0
+};
+
+struct Assembled {
+  bool valid = false;
+  DBuf<double> omega, gphi;       // [K+1][NE]
+  DBuf<double> omegabar;          // [K][NEbar]
+  DBuf<double> Cd, sr;            // C = cbar s/rho, s/rho  (m)
+  DBuf<double> f, g, h, gt;       // RHS pieces
+  DBuf<double> rhs;               // (f; P gt)  (n+m)
+  DBuf<double> Tv;                // [K][3][W][nbar]
+  double scale = 0;               // ||(f;g;h)||
+  double res_norm = 0;            // ||F||
+};
+
+struct bbot_ctx_impl;
+
+}  // namespace bbot
+
+struct bbot_ctx {
+  bbot::Dev dev;
+  bbot::Reducer red;
+  bbot_solver_opts opts;
+  std::string err;
+  bbot::Geometry hg;           // host geometry (kept for inspection)
+  bbot::DevGeom g;
+  // state
+  bbot::DBuf<double> phi, rho_ext, s;
+  double mu = 1.0;
+  bbot::Assembled as;
+  bbot::AmgHierarchy amgA, amgT;
+  bbot::AmgWork amgw;
+  // direction
+  bool have_dir = false;
+  bbot::DBuf<double> sol, dphi, drho, ds;
+  // workspaces
+  bbot::Fgmres outer, innerT;
+  bbot::PcgSlices pcg;
+  bbot::DBuf<double> tmp_n, tmp_n2, tmp_m, tmp_m2, tmp_nm, tmp_nm2;
+  bbot::DBuf<double> scal;      // device scalars / per-slice scratch (>= 8*(K+2))
+  bbot::DBuf<long long> scan_ws;
+  // counters for the current solve
+  int bb_T_its = 0, bb_A_max = 0;
+  long long bb_A_total = 0;
+  long long n() const { return (long long)g.N * (g.K + 1); }
+  long long m() const { return (long long)g.nbar * g.K; }
+};

@@ -1,0 +1,413 @@
+// ops.cu -- a2 (J_P matvec), pieces of the BB apply (a4), recovery (a6),
+// Newton update (a7) and the kinetic energy (D12).
+//
+// Slice conventions (0-based): phi slice kk = 0..K holds phi^{kk+1}; state rho
+// slice k0 = 0..K-1 holds rho^{k0+1}; rho_ext slice j holds rho^j (j = 0..K+1).
+#include "ops.cuh"
+
+namespace bbot {
+
+constexpr int BS = 256;
+
+// ---------------------------------------------------------------- generic reductions
+struct WSlice {          // sum_i w_i x[k][i]   (w = nullptr -> 1)
+  const double* w;
+  const double* x;
+  long long L;
+  __device__ double operator()(int k, long long i) const {
+    double v = x[(size_t)k * L + i];
+    return w ? w[i] * v : v;
+  }
+};
+
+__global__ void k_sub_slice(long long L, int ns, double* __restrict__ x, const double* __restrict__ S,
+                            double scale) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L * ns) return;
+  x[t] -= S[t / L] * scale;
+}
+// x -= w_i S[k] * scale
+__global__ void k_sub_slice_w(long long L, int ns, double* __restrict__ x, const double* __restrict__ w,
+                              const double* __restrict__ S, double scale) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L * ns) return;
+  long long k = t / L;
+  x[t] -= w[t - k * L] * S[k] * scale;
+}
+
+void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L) {
+  double* S = c->scal.p;
+  c->red.slice_sum(WSlice{nullptr, x, L}, L, ns, S, false);
+  launch(c->dev, k_sub_slice, dim3(nblocks(L * ns, BS)), dim3(BS), 0, L, ns, x, (const double*)S, 1.0 / (double)L);
+}
+
+// ---------------------------------------------------------------- B row (coarse)
+// (B x)^k_i, k = k0+1 (1-based):  Pi^T M (x^{k+1} - x^k)/dt
+//   + 1/2 sum_{sigma in E(i)} R_E[sigma,i] |e| [g^k (x^k_L - x^k_R) + g^{k+1} (x^{k+1}_L - x^{k+1}_R)]  (D5, A5)
+struct BRow {
+  int N, NE, nbar;
+  double dt;
+  const double *cf, *gphi, *ce_coef, *e_len;
+  const int *ce_edge, *eL, *eR;
+  __device__ double operator()(const double* x, int k0, long long i) const {
+    const double* x0 = x + (size_t)k0 * N;
+    const double* x1 = x + (size_t)(k0 + 1) * N;
+    double tt = 0.0;
+    for (int q = 0; q < 3; q++) {
+      long long f = 3 * i + q;
+      tt += cf[f] * (x1[f] - x0[f]);
+    }
+    tt /= dt;
+    const double* g0 = gphi + (size_t)k0 * NE;
+    const double* g1 = gphi + (size_t)(k0 + 1) * NE;
+    double sp = 0.0;
+    for (int q = 0; q < CE_MAX; q++) {
+      int e = ce_edge[(size_t)q * nbar + i];
+      if (e < 0) break;
+      int L = eL[e], R = eR[e];
+      sp += ce_coef[(size_t)q * nbar + i] * e_len[e] * (g0[e] * (x0[L] - x0[R]) + g1[e] * (x1[L] - x1[R]));
+    }
+    return tt + 0.5 * sp;
+  }
+};
+
+// (B^T u)^k_f, k = kk+1:  M Pi (u^{k-1} - u^k)/dt + 1/2 sum_{sigma ni f} E[f,sigma] |e| g^k (R_E (u^{k-1}+u^k))_sigma
+// u given as y (state layout) minus a per-slice constant shift[k0]*sc (P^T), shift may be null.  (D6)
+struct BtRow {
+  int N, NE, nbar, K;
+  double dt;
+  const double *cf, *gphi, *e_len, *lam;
+  const int *fe, *eL, *eR;
+  __device__ double operator()(const double* y, const double* shift, double sc, int kk, long long f) const {
+    auto u = [&](int k0, int j) -> double {
+      if (k0 < 0 || k0 >= K) return 0.0;
+      double v = y[(size_t)k0 * nbar + j];
+      return shift ? v - shift[k0] * sc : v;
+    };
+    int pf = (int)(f / 3);
+    double tt = cf[f] * (u(kk - 1, pf) - u(kk, pf)) / dt;
+    const double* gk = gphi + (size_t)kk * NE;
+    double sp = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      int e = fe[t * N + f];
+      if (e < 0) continue;
+      int L = eL[e], R = eR[e];
+      int pL = L / 3, pR = R / 3;
+      double l = lam[e];
+      double ru = l * (u(kk - 1, pL) + u(kk, pL)) + (1.0 - l) * (u(kk - 1, pR) + u(kk, pR));
+      double sgn = (L == f) ? 1.0 : -1.0;
+      sp += sgn * e_len[e] * gk[e] * ru;
+    }
+    return tt + 0.5 * sp;
+  }
+};
+
+static BRow make_brow(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  return BRow{g.N, g.NE, g.nbar, g.dt, g.c.p, c->as.gphi.p, g.ce_coef.p, g.e_len.p, g.ce_edge.p, g.eL.p, g.eR.p};
+}
+static BtRow make_btrow(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  return BtRow{g.N, g.NE, g.nbar, g.K, g.dt, g.c.p, c->as.gphi.p, g.e_len.p, g.lam.p, g.fadj_e.p, g.eL.p, g.eR.p};
+}
+
+// ---------------------------------------------------------------- a2: J_P
+__global__ void k_jp_y1(long long n, int N, int NE, const double* __restrict__ omega, const int* __restrict__ fe,
+                        const int* __restrict__ fnb, BtRow bt, const double* __restrict__ x1,
+                        const double* __restrict__ x2, const double* __restrict__ S, double inv_area,
+                        double* __restrict__ y1) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int kk = (int)(t / N);
+  long long f = t - (long long)kk * N;
+  const double* xs = x1 + (size_t)kk * N;
+  const double* om = omega + (size_t)kk * NE;
+  double xf = xs[f], acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    int e = fe[q * N + f];
+    if (e >= 0) acc += om[e] * (xf - xs[fnb[q * N + f]]);
+  }
+  y1[t] = acc + bt(x2, S, inv_area, kk, f);     // A x1 + B^T P^T x2
+}
+
+struct JpT {   // t = B x1 - C P^T x2, stored; returns t (for P)
+  BRow br;
+  const double *x1, *x2, *S, *Cd;
+  double inv_area;
+  double* out;
+  int nbar;
+  __device__ double operator()(int k0, long long i) const {
+    size_t t = (size_t)k0 * nbar + i;
+    double u = x2[t] - S[k0] * inv_area;
+    double v = br(x1, k0, i) - Cd[t] * u;
+    out[t] = v;
+    return v;
+  }
+};
+
+void jp_matvec(bbot_ctx* c, const double* x, double* y) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  int K = g.K;
+  const double* x1 = x;
+  const double* x2 = x + n;
+  double* S1 = c->scal.p;            // c-bar weighted slice sums of x2 (P^T)
+  double* S2 = c->scal.p + (K + 2);  // plain slice sums of t (P)
+  c->red.slice_sum(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, K, S1, false);
+  launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, g.NE, (const double*)c->as.omega.p,
+         (const int*)g.fadj_e.p, (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
+         1.0 / g.area, y);
+  c->red.slice_sum(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, K, S2, false);
+  launch(c->dev, k_sub_slice_w, dim3(nblocks(m, BS)), dim3(BS), 0, (long long)g.nbar, K, y + n,
+         (const double*)g.cbar.p, (const double*)S2, 1.0 / g.area);
+}
+
+// ---------------------------------------------------------------- y = T x, y = A x
+template <class V>
+__global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= v.nrows) return;
+  double acc = 0.0;
+  v.row(r, [&](long long col, double a) { acc += a * x[col]; });
+  y[r] = acc;
+}
+
+void apply_T(bbot_ctx* c, const double* x, double* y) {
+  SliceEllView v = view_T(c);
+  launch(c->dev, k_spmv<SliceEllView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
+}
+void apply_A(bbot_ctx* c, const double* x, double* y) {
+  EdgeLapView v = view_A(c);
+  launch(c->dev, k_spmv<EdgeLapView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
+}
+
+// ---------------------------------------------------------------- a4 pieces
+struct AtZ {   // v = (Atilde_k z)_i / cbar_i, stored; returns cbar_i v (for P^T)
+  int nbar, NEbar;
+  const double *z, *omegabar, *cbar;
+  const int *cadj_e, *cadj_nb;
+  double* out;
+  __device__ double operator()(int k0, long long i) const {
+    const double* zs = z + (size_t)k0 * nbar;
+    const double* ob = omegabar + (size_t)k0 * NEbar;
+    double zi = zs[i], acc = 0.0;
+    for (int t = 0; t < 3; t++) {
+      int e = cadj_e[t * nbar + i];
+      if (e >= 0) acc += ob[e] * (zi - zs[cadj_nb[t * nbar + i]]);
+    }
+    double v = acc / cbar[i];
+    out[(size_t)k0 * nbar + i] = v;
+    return cbar[i] * v;
+  }
+};
+
+void bb_y_from_z(bbot_ctx* c, const double* z, double* y) {
+  DevGeom& g = c->g;
+  double* S = c->scal.p;
+  c->red.slice_sum(AtZ{g.nbar, g.NEbar, z, c->as.omegabar.p, g.cbar.p, g.cadj_e.p, g.cadj_nb.p, y}, g.nbar, g.K, S,
+                   false);
+  launch(c->dev, k_sub_slice, dim3(nblocks(c->m(), BS)), dim3(BS), 0, (long long)g.nbar, g.K, y, (const double*)S,
+         1.0 / g.area);
+}
+
+struct RhsA {  // b = r1 - B^T y, stored; returns b
+  BtRow bt;
+  const double *r1, *y;
+  double* out;
+  int N;
+  __device__ double operator()(int kk, long long f) const {
+    size_t t = (size_t)kk * N + f;
+    double v = r1[t] - bt(y, nullptr, 0.0, kk, f);
+    out[t] = v;
+    return v;
+  }
+};
+
+void bb_rhs_A(bbot_ctx* c, const double* r1, const double* y, double* b) {
+  DevGeom& g = c->g;
+  double* S = c->scal.p;
+  c->red.slice_sum(RhsA{make_btrow(c), r1, y, b, g.N}, g.N, g.K + 1, S, false);
+  launch(c->dev, k_sub_slice, dim3(nblocks(c->n(), BS)), dim3(BS), 0, (long long)g.N, g.K + 1, b, (const double*)S,
+         1.0 / (double)g.N);
+}
+
+// ---------------------------------------------------------------- a6 recovery
+struct QSum {  // q = g~ - B dphit + C drho ; returns q
+  BRow br;
+  const double *dphit, *drho, *gt, *Cd;
+  int nbar;
+  __device__ double operator()(int k0, long long i) const {
+    size_t t = (size_t)k0 * nbar + i;
+    return gt[t] - br(dphit, k0, i) + Cd[t] * drho[t];
+  }
+};
+
+__global__ void k_prefix_shift(int K, double dt, double inv_area, const double* __restrict__ qs, double* shift) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double acc = 0.0;
+  shift[0] = 0.0;
+  for (int j = 0; j < K; j++) {
+    acc += dt * (qs[j] * inv_area);      // sum_{i<k} dt dlambda^i  (4.15, A10)
+    shift[j + 1] = acc;
+  }
+}
+
+__global__ void k_add_shift(long long n, int N, const double* __restrict__ src, const double* __restrict__ shift,
+                            double* __restrict__ dst) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  dst[t] = src[t] + shift[t / N];
+}
+
+__global__ void k_ds(long long m, const double* __restrict__ h, const double* __restrict__ s,
+                     const double* __restrict__ drho, const double* __restrict__ rho, double* __restrict__ ds) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  ds[t] = (h[t] - s[t] * drho[t]) / rho[t];
+}
+
+void recover(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  int K = g.K;
+  cudaStream_t s = c->dev.stream;
+  double* S = c->scal.p;
+  double* shift = c->scal.p + 2 * (K + 2);
+  // drho = P^T y  (A30)
+  BB_CUDA(cudaMemcpyAsync(c->drho.p, c->sol.p + n, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  c->red.slice_sum(WSlice{g.cbar.p, c->drho.p, g.nbar}, g.nbar, K, S, false);
+  launch(c->dev, k_sub_slice, dim3(nblocks(m, BS)), dim3(BS), 0, (long long)g.nbar, K, c->drho.p, (const double*)S,
+         1.0 / g.area);
+  // dphit -= c^T dphit^k / |Omega|  (A11), kept in tmp_n
+  double* dphit = c->tmp_n.p;
+  BB_CUDA(cudaMemcpyAsync(dphit, c->sol.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  c->red.slice_sum(WSlice{g.c.p, dphit, g.N}, g.N, K + 1, S, false);
+  launch(c->dev, k_sub_slice, dim3(nblocks(n, BS)), dim3(BS), 0, (long long)g.N, K + 1, dphit, (const double*)S,
+         1.0 / g.area);
+  // dlambda = E-bar(g~ - B dphit + C drho)/|Omega|
+  c->red.slice_sum(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar}, g.nbar, K, S, false);
+  launch(c->dev, k_prefix_shift, dim3(1), dim3(32), 0, K, g.dt, 1.0 / g.area, (const double*)S, shift);
+  launch(c->dev, k_add_shift, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)dphit, (const double*)shift,
+         c->dphi.p);
+  launch(c->dev, k_ds, dim3(nblocks(m, BS)), dim3(BS), 0, m, (const double*)c->as.h.p, (const double*)c->s.p,
+         (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p);
+}
+
+// ---------------------------------------------------------------- a7 update
+struct RatioMin {
+  long long m;
+  const double *rho, *drho, *s, *ds;
+  __device__ double operator()(int, long long i) const {
+    double x, d;
+    if (i < m) { x = rho[i]; d = drho[i]; }
+    else { x = s[i - m]; d = ds[i - m]; }
+    return d < 0.0 ? -x / d : 1e300;
+  }
+};
+
+__global__ void k_update(long long n, long long m, double tau, const double* __restrict__ minv,
+                         double* __restrict__ phi, double* __restrict__ rho, double* __restrict__ s,
+                         const double* __restrict__ dphi, const double* __restrict__ drho,
+                         const double* __restrict__ ds, double* __restrict__ alpha_out) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double mv = *minv;
+  double a = 1.0;
+  if (mv < 1e299) a = fmin(1.0, tau * mv);       // A20
+  if (t == 0) *alpha_out = a;
+  if (t < n) phi[t] += a * dphi[t];
+  else if (t < n + m) rho[t - n] += a * drho[t - n];
+  else if (t < n + 2 * m) s[t - n - m] += a * ds[t - n - m];
+}
+
+__global__ void k_renorm(long long m, int nbar, double target, const double* __restrict__ mass,
+                         double* __restrict__ rho) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  rho[t] = rho[t] * (target / mass[t / nbar]);   // Remark 3.2
+}
+
+double newton_update(bbot_ctx* c, double tau) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  double* S = c->scal.p;
+  double* rho = c->rho_ext.p + g.nbar;
+  c->red.slice_min(RatioMin{m, rho, c->drho.p, c->s.p, c->ds.p}, 2 * m, 1, S + 3 * (g.K + 2));
+  launch(c->dev, k_update, dim3(nblocks(n + 2 * m, BS)), dim3(BS), 0, n, m, tau, (const double*)(S + 3 * (g.K + 2)),
+         c->phi.p, rho, c->s.p, (const double*)c->dphi.p, (const double*)c->drho.p, (const double*)c->ds.p,
+         S + 3 * (g.K + 2) + 1);
+  // target mass c-bar^T rho^0
+  c->red.slice_sum(WSlice{g.cbar.p, c->rho_ext.p, g.nbar}, g.nbar, 1, S + 3 * (g.K + 2) + 2, false);
+  c->red.slice_sum(WSlice{g.cbar.p, rho, g.nbar}, g.nbar, g.K, S, false);
+  double target = read_scalar(c->dev, S + 3 * (g.K + 2) + 2);
+  launch(c->dev, k_renorm, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, target, (const double*)S, rho);
+  c->as.valid = false;
+  return read_scalar(c->dev, S + 3 * (g.K + 2) + 1);
+}
+
+// ---------------------------------------------------------------- D12
+struct KeF {
+  int N, NE, nbar;
+  const int *eL, *eR;
+  const double *lam, *e_len, *w_len, *phi, *rho_ext;
+  __device__ double operator()(int kk, long long e) const {
+    int L = eL[e], R = eR[e];
+    int pL = L / 3, pR = R / 3;
+    const double* ra = rho_ext + (size_t)(kk + 1) * nbar;
+    const double* rb = rho_ext + (size_t)kk * nbar;
+    double l = lam[e];
+    double rt = l * (0.5 * (ra[pL] + rb[pL])) + (1.0 - l) * (0.5 * (ra[pR] + rb[pR]));
+    double dphi = phi[(size_t)kk * N + L] - phi[(size_t)kk * N + R];
+    return e_len[e] * rt / w_len[e] * dphi * dphi;       // phi^T A_k phi edge by edge
+  }
+};
+
+double kinetic_energy(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  double* S = c->scal.p;
+  c->red.slice_sum(KeF{g.N, g.NE, g.nbar, g.eL.p, g.eR.p, g.lam.p, g.e_len.p, g.w_len.p, c->phi.p, c->rho_ext.p},
+                   g.NE, g.K + 1, S, false);
+  std::vector<double> h(g.K + 1);
+  BB_CUDA(cudaMemcpyAsync(h.data(), S, (g.K + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->dev.stream));
+  sync(c->dev);
+  double ke = 0.0;
+  for (double v : h) ke += g.dt * 0.5 * v;
+  return ke;
+}
+
+// ---------------------------------------------------------------- state helpers
+__global__ void k_init_state(long long n, long long m, double rho0, double mu0, double* phi, double* rho, double* s) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) phi[t] = 0.0;
+  if (t < m) { rho[t] = rho0; s[t] = mu0 / rho0; }
+}
+
+void init_state(bbot_ctx* c, double mu0) {
+  DevGeom& g = c->g;
+  double* S = c->scal.p;
+  c->red.slice_sum(WSlice{g.cbar.p, c->rho_ext.p, g.nbar}, g.nbar, 1, S, false);
+  double mass = read_scalar(c->dev, S);
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_init_state, dim3(nblocks(std::max(n, m), BS)), dim3(BS), 0, n, m, mass / g.area, mu0, c->phi.p,
+         c->rho_ext.p + g.nbar, c->s.p);
+  c->mu = mu0;
+  c->as.valid = false;
+  c->have_dir = false;
+}
+
+struct PosMin {
+  long long m;
+  const double *rho, *s;
+  __device__ double operator()(int, long long i) const { return i < m ? rho[i] : s[i - m]; }
+};
+
+void check_state(bbot_ctx* c) {
+  long long m = c->m();
+  double* S = c->scal.p;
+  c->red.slice_min(PosMin{m, c->rho_ext.p + c->g.nbar, c->s.p}, 2 * m, 1, S);
+  double mn = read_scalar(c->dev, S);
+  BB_REQUIRE(mn > 0.0, BBOT_E_STATE, "state has rho <= 0 or s <= 0");
+}
+
+}  // namespace bbot

@@ -1,0 +1,33 @@
+// ops.cuh -- declarations of the per-Newton-step kernels (assemble.cu, ops.cu)
+// and of the solver orchestration (solver.cu).
+#pragma once
+#include "ctx.cuh"
+
+namespace bbot {
+
+// assemble.cu
+void upload_geometry(bbot_ctx* c, const Geometry& g, int K);
+void assemble_edges(bbot_ctx* c);                    // omega, gphi, omegabar, C, s/rho
+void compute_residual(bbot_ctx* c, bool write_rhs);  // F (as f,g,h = -F), g~, rhs, norms
+void assemble_T(bbot_ctx* c);                        // T values
+EdgeLapView view_A(bbot_ctx* c);
+SliceEllView view_T(bbot_ctx* c);
+
+// ops.cu
+void jp_matvec(bbot_ctx* c, const double* x, double* y);                    // (4.17)
+void apply_T(bbot_ctx* c, const double* x, double* y);                      // y = T x
+void bb_y_from_z(bbot_ctx* c, const double* z, double* y);                  // y = P^T Mbar^-1 Atilde z
+void bb_rhs_A(bbot_ctx* c, const double* r1, const double* y, double* b);   // b = r1 - B^T y, slice means removed
+void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L);         // arithmetic mean per slice
+void recover(bbot_ctx* c);                                                   // a6
+double newton_update(bbot_ctx* c, double tau);                              // a7 step + renormalise
+double kinetic_energy(bbot_ctx* c);
+void init_state(bbot_ctx* c, double mu0);
+void check_state(bbot_ctx* c);
+
+// solver.cu
+void assemble_all(bbot_ctx* c, bbot_solve_stats* st);
+void bb_apply(bbot_ctx* c, const double* r, double* z);
+void solve(bbot_ctx* c, bbot_solve_stats* st);
+
+}  // namespace bbot

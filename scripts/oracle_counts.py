@@ -1,0 +1,39 @@
+"""Write tests/golden/oracle_counts.json: the oracle's own FGMRES outer-iteration
+counts on the bench systems (calls only oracle/ and synthetic/).  Used by
+bench.py to scale the bounded oracle sample (setup + 3 outer iterations) to a
+full Newton solve for the cpu_baseline / reference arm."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+from oracle.bb import BBSolver, SolverOpts  # noqa: E402
+from oracle.ops import Discretisation  # noqa: E402
+from synthetic import initial_state, make_problem  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
+
+
+def main(names):
+    data = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    for name in names:
+        p = make_problem(name)
+        d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+        phi, rho, s = initial_state(p, 1.0)
+        t = time.time()
+        with threadpool_limits(1):
+            S = BBSolver(d, phi, rho, s, 1.0, SolverOpts())
+            S.solve()
+        key = f"{name}/init/mu=1"
+        data[key] = dict(outer_its=S.stats["outer_its"], inner_T_its=S.stats["inner_T_its"],
+                         converged=S.stats["converged"], seconds_1core=round(time.time() - t, 1))
+        print(key, data[key], flush=True)
+        json.dump(data, open(OUT, "w"), indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["C1", "C2"])

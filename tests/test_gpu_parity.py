@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on
+identical seeded inputs.  Tolerances:
+  operators (residual, J_P, T): relative 1e-12 in max norm (fp64, different
+    summation order only);
+  AMG aggregates: identical integers;  V-cycle: 1e-10;
+  Newton direction: relative 1e-8 per block (north star);  counts +-1;
+  kinetic energy after a full IPM: relative 1e-6 (north star).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import amg as oamg                       # noqa: E402
+from oracle.bb import BBSolver, SolverOpts           # noqa: E402
+from oracle.ops import Discretisation                # noqa: E402
+from synthetic import initial_state, make_problem, random_state   # noqa: E402
+
+
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2209_00315_b200 as pb
+    return pb
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def _setup(name, state="random", mu=1e-2, seed=3, **kw):
+    pb = _gpu()
+    p = make_problem(name, **kw)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    if state == "random":
+        phi, rho, s = random_state(p, seed=seed, mu=mu)
+    else:
+        phi, rho, s = initial_state(p, mu)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, mu)
+    return pb, p, d, ctx, (phi, rho, s, mu)
+
+
+CASES = [("T1", {}), ("C1", {}), ("T2b", {})]
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_residual_parity(name, kw):
+    pb, p, d, ctx, (phi, rho, s, mu) = _setup(name, **kw)
+    Fp, Fr, Fs, nrm = ctx.residual()
+    op, orr, os_ = d.residual(phi, rho, s, mu)
+    assert _rel(Fp, op) < 1e-12 and _rel(Fr, orr) < 1e-12 and _rel(Fs, os_) < 1e-12
+    ref = np.sqrt(op @ op + orr @ orr + os_ @ os_)
+    assert abs(nrm - ref) <= 1e-12 * ref
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_T_and_JP_parity(name, kw):
+    """T = C M̄^{-1} Ã - B M^{-1} B̃ (4.26) entrywise, and J_P x (4.17)."""
+    import scipy.sparse as sp
+    pb, p, d, ctx, (phi, rho, s, mu) = _setup(name, **kw)
+    ctx.assemble()
+    rp, ci, cv = ctx.get_T()
+    Tg = sp.csr_matrix((cv, ci, rp), shape=(d.m, d.m))
+    To = d.T_matrix(phi, rho, s)
+    diff = abs(Tg - To).max()
+    assert diff <= 1e-12 * abs(To).max()
+    JP, *_ = d.make_JP(phi, rho, s)
+    x = np.random.default_rng(11).standard_normal(d.n + d.m)
+    assert _rel(ctx.jp_matvec(x), JP(x)) < 1e-12
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_amg_aggregates_identical_and_vcycle(name, kw):
+    """I3 on both sides: identical aggregates level by level; V-cycle parity."""
+    pb, p, d, ctx, (phi, rho, s, mu) = _setup(name, **kw)
+    ctx.assemble()
+    S = BBSolver(d, phi, rho, s, mu, SolverOpts())
+    for which, H in ((0, S.amgA), (1, S.amgT)):
+        sizes = ctx.amg_info(which)
+        assert sizes == H.sizes, (which, sizes, H.sizes)
+        for lvl in range(len(sizes) - 1):
+            assert np.array_equal(ctx.amg_agg(which, lvl), H.levels[lvl].agg), (which, lvl)
+        b = np.random.default_rng(5 + which).standard_normal(sizes[0])
+        if which == 0:                       # consistent right-hand side per slice
+            B = b.reshape(d.K + 1, d.N)
+            b = (B - B.mean(1, keepdims=True)).reshape(-1)
+        xg = ctx.amg_vcycle(which, b)
+        xo = oamg.vcycle(H, b)
+        # the coarsest T level is a dense inverse (Gauss-Jordan vs LAPACK) of an
+        # ill-conditioned matrix: agreement is bounded by cond * eps, not eps
+        assert _rel(xg, xo) < (1e-10 if which == 0 else 2e-9), (which, _rel(xg, xo))
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_bb_apply_parity(name, kw):
+    pb, p, d, ctx, (phi, rho, s, mu) = _setup(name, **kw)
+    ctx.assemble()
+    S = BBSolver(d, phi, rho, s, mu, SolverOpts())
+    r = np.random.default_rng(9).standard_normal(d.n + d.m)
+    r[d.n:] = d.P(r[d.n:])
+    zg, itT, itA = ctx.bb_apply(r)
+    zo = S.apply(r)
+    assert itT == S.inner_T_its and itA == int(S.inner_A_its[-1].max())
+    assert _rel(zg, zo) < 1e-8
+
+
+_IPM_CACHE = {}
+
+
+def ipm_state(name, mu_target, **kw):
+    """A realistic Newton system: the oracle's own IPM trajectory (A17-A20) from
+    the A19 point, stopped after the mu = mu_target step (inputs never come from
+    the CUDA path)."""
+    from oracle.ipm import IpmOpts, ipm_run
+    key = (name, mu_target, tuple(sorted(kw.items())))
+    if key not in _IPM_CACHE:
+        p = make_problem(name, **kw)
+        d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+        phi, rho, s = initial_state(p, 1.0)
+        if mu_target < 1.0:
+            r = ipm_run(d, phi, rho, s, IpmOpts(mu_min=mu_target), SolverOpts())
+            phi, rho, s = r.phi, r.rho, r.s
+        _IPM_CACHE[key] = (p, d, phi, rho, s)
+    return _IPM_CACHE[key]
+
+
+@pytest.mark.parametrize("name,mu", [("T1", 2.0 ** -6), ("T2", 1.0), ("T2", 2.0 ** -8), ("C1", 1.0),
+                                     ("C1", 2.0 ** -3), ("T2b", 2.0 ** -5)])
+def test_newton_direction_parity(name, mu):
+    """North star: each Newton direction to relative 1e-8, outer counts +-1, on
+    states of the IPM trajectory (the next system the IPM would solve, at mu/2)."""
+    pb = _gpu()
+    p, d, phi, rho, s = ipm_state(name, mu)
+    mu_sys = mu / 2 if mu < 1.0 else 1.0
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, mu_sys)
+    ctx.assemble()
+    dphi, drho, ds, st = ctx.solve()
+    S = BBSolver(d, phi, rho, s, mu_sys, SolverOpts())
+    ophi, orho, os_ = S.solve()
+    assert S.stats["converged"], S.stats
+    assert abs(st["outer_its"] - S.stats["outer_its"]) <= 1, (st, S.stats)
+    assert st["converged"] == 1
+    for a, b in ((dphi, ophi), (drho, orho), (ds, os_)):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_newton_update_and_ke_parity():
+    """a7 step (alpha, update, renormalisation) and D12."""
+    from oracle.ipm import renormalise, step_length
+    pb = _gpu()
+    p, d, phi, rho, s = ipm_state("C1", 2.0 ** -3)
+    mu = 2.0 ** -4
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, mu)
+    ctx.assemble()
+    dphi, drho, ds, st = ctx.solve()
+    a = ctx.newton_update(0.95)
+    ao = step_length(rho, s, drho, ds, 0.95)
+    assert abs(a - ao) <= 1e-14 * ao
+    phi2, rho2, s2, _ = ctx.get_state()
+    assert _rel(phi2, phi + ao * dphi) < 1e-13
+    assert _rel(rho2, renormalise(d, rho + ao * drho)) < 1e-13
+    assert _rel(s2, s + ao * ds) < 1e-13
+    assert abs(ctx.kinetic_energy() - d.kinetic_energy(phi2, rho2)) <= 1e-12 * d.kinetic_energy(phi2, rho2)
+
+
+def test_ipm_parity_T1():
+    """Full IPM (mu 1 -> 2^-12, A17-A20) on both sides: every system's outer count
+    +-1 and the final kinetic energy to 1e-6 (north star)."""
+    from oracle.ipm import IpmOpts, ipm_run
+    pb = _gpu()
+    p = make_problem("T1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    res = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -12), SolverOpts())
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=2.0 ** -12))
+    assert st["n_systems"] == len(res.log)
+    for g, o in zip(log, res.log):
+        assert abs(g["outer_its"] - o["outer_its"]) <= 1
+    assert abs(st["kinetic_energy"] - res.kinetic_energy) <= 1e-6 * abs(res.kinetic_energy)
+    phi2, rho2, s2, _ = ctx.get_state()
+    assert np.linalg.norm(rho2 - res.rho) <= 1e-6 * np.linalg.norm(res.rho)
+
+
+def test_state_errors():
+    pb = _gpu()
+    p = make_problem("T0")
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    rho[3] = -1.0
+    with pytest.raises(pb.BbotError):
+        ctx.set_state(phi, rho, s, 1.0)
+    ctx2 = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    with pytest.raises(pb.BbotError):
+        ctx2.solve()          # before assemble -> BBOT_E_ORDER
