@@ -103,24 +103,34 @@ class ClockSampler:
 
 
 def byte_models(ctx, nnzT):
-    """Algorithmic (compulsory) bytes per launch of the main kernels."""
+    """Algorithmic (compulsory) bytes per launch of the main kernels.
+    fp64 = 8 B, int32 = 4 B; geometry tables shared by all time slices count once."""
     n, m, N, NE, K, nbar = ctx.n, ctx.m, ctx.N, ctx.NE, ctx.K, ctx.nbar
     W = ctx.T_width
     A_sizes, T_sizes = ctx.amg_info(0), ctx.amg_info(1)
     nc1A = A_sizes[1] if len(A_sizes) > 1 else 0
     nc1T = T_sizes[1] if len(T_sizes) > 1 else 0
-    om = 8 * (K + 1) * NE + 32 * N          # edge weights + cell->edge tables (once)
+    om = 8 * (K + 1) * NE + 32 * N          # edge weights omega + cell->edge tables [4][N] x2 (once)
     tT = 8 * nnzT + 4 * W * nbar            # T values + shared column pattern
     return {
+        # per-slice PCG (I4): p = z + beta p, q = A z + beta q, p.q   (reads z p q, writes p q)
+        "void bbot::k_pcg_pq<bbot::EdgeLapView>": 40 * n + om,
+        "bbot::k_pcg_xr": 48 * n,                      # x += a p, r -= a q, r.r
+        "bbot::k_pcg_rz": 16 * n,
         "void bbot::k_spmv<bbot::EdgeLapView>": 16 * n + om,
         "void bbot::k_down<bbot::EdgeLapView>": 32 * n + om,
         "void bbot::k_up<bbot::EdgeLapView>": 36 * n + 8 * nc1A + om,
         "void bbot::k_spmv<bbot::SliceEllView>": tT + 16 * m,
         "void bbot::k_down<bbot::SliceEllView>": tT + 32 * m,
         "void bbot::k_up<bbot::SliceEllView>": tT + 36 * m + 8 * nc1T,
-        "bbot::k_pcg_xr(long long, int, double const*, double*, double*, double const*, double const*)": 48 * n,
-        "bbot::k_pcg_p(long long, int, double const*, double const*, double*)": 24 * n,
     }
+
+
+def _match_model(name, models):
+    for k in models:
+        if name == k or name.startswith(k + "("):
+            return k
+    return None
 
 
 def oracle_sample(config, n_outer_sample=3):
@@ -230,7 +240,6 @@ def main():
         dist.barrier()
     clk = ClockSampler(local_rank)
     clk.start()
-    l0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     e0.record(stream)
@@ -242,7 +251,6 @@ def main():
         dist.barrier()
     clocks = clk.stop()
     t = e0.elapsed_time(e1) / 1e3
-    launches = (ctx.launch_count() - l0) // args.steps
     if dist is not None:
         tt = torch.tensor([t], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -276,34 +284,41 @@ def main():
         te = float(tt.item())
     io_bytes = 8 * (ctx.n + 2 * ctx.m)
 
-    # ---- per-kernel shares (one extra profiled step, CUDA events around every launch)
+    # ---- per-kernel shares: one extra step of the same system issued eagerly (the
+    # per-launch profiler brackets every kernel with CUDA events on the launching
+    # stream).  The eager issue runs exactly the kernels the graph replays
+    # (bitwise-identical results), so its launch count is the step's launch count.
     roof = None
     prof_table = None
+    launches = None
     if not args.no_profile:
+        l0 = ctx.launch_count()
         ctx.prof_start()
         step()
         prof_table = ctx.prof_stop()
+        launches = ctx.launch_count() - l0
         nnzT, _ = ctx.T_nnz()
         models = byte_models(ctx, nnzT)
         total_ms = sum(v[1] for v in prof_table.values())
         ranked = sorted(prof_table.items(), key=lambda kv: -kv[1][1])
-        dom = next(((k, v) for k, v in ranked if k in models), None)
+        dom = next(((k, v) for k, v in ranked if _match_model(k, models)), None)
         peak, peak_kind = hbm_peak()
         if dom is not None:
             name, (cnt, ms) = dom
             avg_s = ms / cnt / 1e3
-            ach = models[name] / avg_s / 1e9
+            model = models[_match_model(name, models)]
+            ach = model / avg_s / 1e9
             traffic = None
             try:
                 summ = json.load(open(NCU_SUMMARY))
-                traffic = summ.get("dram_bytes_per_launch", {}).get(name)
+                traffic = summ.get("dram_bytes_per_launch", {}).get(_match_model(name, models))
             except Exception:
                 pass
             roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                    "algorithmic_bytes_per_launch": models[name], "avg_launch_us": round(avg_s * 1e6, 2),
-                    "share_of_step": round(ms / total_ms, 4), "top_kernel": ranked[0][0],
-                    "top_kernel_share": round(ranked[0][1][1] / total_ms, 4)}
+                    "algorithmic_bytes_per_launch": model, "avg_launch_us": round(avg_s * 1e6, 2),
+                    "launches_per_step": cnt, "share_of_step": round(ms / total_ms, 4),
+                    "top_kernel": ranked[0][0], "top_kernel_share": round(ranked[0][1][1] / total_ms, 4)}
         if args.profile_out and rank == 0:
             json.dump({"config": args.config, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in ranked},
                        "total_ms": total_ms, "models": models}, open(args.profile_out, "w"), indent=1)
@@ -332,7 +347,8 @@ def main():
                                          "amg_levels_A", "amg_levels_T")},
             "e2e": {"value": world * args.steps / te, "unit": "solves/s", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches) if launches is not None else None,
+            "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms", "t_graph_ms")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clocks,

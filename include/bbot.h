@@ -54,9 +54,9 @@ typedef struct {
   double eps_out;      /* outer FGMRES tol on ||res(4.17)|| / ||(f;g;h)|| [1e-10] (A16) */
   double eps_T;        /* inner GMRES tol for T z = -r2, relative [1e-1]           */
   double eps_A;        /* inner PCG tol for A_k x = b, relative [1e-3] (A14; paper 5e-2)    */
-  int restart;         /* FGMRES restart [30] (A15)                                         */
+  int restart;         /* FGMRES restart [30] (A15), 1..32                                  */
   int maxit;           /* FGMRES cap [400]                                         */
-  int restart_T;       /* inner GMRES restart [10]                                          */
+  int restart_T;       /* inner GMRES restart [10], 1..32                                   */
   int maxit_inner;     /* inner caps (T GMRES total its, per-slice PCG its) [50]            */
   double omega_A;      /* damped-Jacobi weight, AMG(A) [2/3]                                */
   double omega_T;      /* damped-Jacobi weight, AMG(T) [0.7]                                */
@@ -75,8 +75,9 @@ typedef struct {
   double t_assemble_ms;     /* a1 + T assembly                                              */
   double t_setup_ms;        /* AMG(A) + AMG(T) setup (the paper's "% preprocess")   */
   double t_krylov_ms;       /* FGMRES incl. BB applies                                      */
-  double t_recover_ms;      /* a6                                                           */
+  double t_recover_ms;      /* a6 (inside the solve graph: 0 when the solve ran as a graph)   */
   int amg_levels_A, amg_levels_T;
+  double t_graph_ms;        /* host time to capture + instantiate the solve graph (0 on replay) */
 } bbot_solve_stats;
 
 typedef struct {
@@ -160,6 +161,7 @@ bbot_status bbot_bb_apply(bbot_ctx* ctx, const double* r, double* z, bbot_mem me
                           int* inner_T_its, int* inner_A_its_max);
 
 /* a5 + a6: FGMRES on (4.17) with the BB preconditioner, then recovery of
+ * (dphi, drho, ds); st also reports the timings of the last bbot_assemble.
  * (dphi, drho, ds) ((4.15) with A10, A30).  Outputs may be
  * NULL (the direction is always kept in the context for bbot_newton_update). */
 bbot_status bbot_solve(bbot_ctx* ctx, double* dphi, double* drho, double* ds,
@@ -185,8 +187,18 @@ bbot_status bbot_amg_info(bbot_ctx* ctx, int which, int* nlevels, long long* siz
 bbot_status bbot_amg_agg(bbot_ctx* ctx, int which, int level, int* agg);
 /* one V-cycle x = M^-1 b on level 0 of hierarchy `which` (length n or m). */
 bbot_status bbot_amg_vcycle(bbot_ctx* ctx, int which, const double* b, double* x, bbot_mem mem);
-/* count of CUDA kernel launches issued by this context since creation. */
+/* count of CUDA kernel launches issued EAGERLY by this context since creation
+ * (kernels replayed from the solve's CUDA graph are not counted; run the same
+ * solve with bbot_set_exec_mode(ctx, 0) or under the profiler to count them). */
 long long bbot_launch_count(const bbot_ctx* ctx);
+/* Execution mode of bbot_solve.  1 (default): the whole solve -- FGMRES, the BB
+ * applies with their inner GMRES / per-slice PCG loops, recovery -- is captured
+ * once per bbot_assemble into one CUDA graph whose loops are conditional WHILE
+ * nodes driven by device-side convergence tests, and replayed with a single
+ * launch (no host round trip inside the solve).  0: the same kernels are issued
+ * eagerly and the host reads each loop condition.  Results are bitwise
+ * identical.  Between bbot_prof_start and bbot_prof_stop solves run eagerly. */
+bbot_status bbot_set_exec_mode(bbot_ctx* ctx, int use_graph);
 /* Per-launch profiler: between start and stop every kernel launch is bracketed
  * by CUDA events on the context stream (adds ~2 event records per launch; use
  * for kernel shares, not for the headline timing).  stop writes a text table

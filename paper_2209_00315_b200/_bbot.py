@@ -32,7 +32,7 @@ class SolveStats(C.Structure):
                 ("inner_A_its_total", C.c_longlong), ("converged", C.c_int), ("rel_res", C.c_double),
                 ("scale", C.c_double), ("t_assemble_ms", C.c_double), ("t_setup_ms", C.c_double),
                 ("t_krylov_ms", C.c_double), ("t_recover_ms", C.c_double),
-                ("amg_levels_A", C.c_int), ("amg_levels_T", C.c_int)]
+                ("amg_levels_A", C.c_int), ("amg_levels_T", C.c_int), ("t_graph_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -93,6 +93,7 @@ _sigs = {
     "bbot_amg_agg": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "bbot_amg_vcycle": (C.c_int, [_P, C.c_int, _P, _P, C.c_int]),
     "bbot_launch_count": (C.c_longlong, [_P]),
+    "bbot_set_exec_mode": (C.c_int, [_P, C.c_int]),
     "bbot_prof_start": (C.c_int, [_P]),
     "bbot_prof_stop": (C.c_int, [_P, C.c_char_p, C.c_longlong, C.POINTER(C.c_longlong)]),
 }
@@ -308,6 +309,10 @@ class Context:
 
     def launch_count(self):
         return lib.bbot_launch_count(self._h)
+
+    def set_exec_mode(self, use_graph: bool):
+        """True: each solve is one CUDA-graph launch (device-side loops); False: eager."""
+        self._check(lib.bbot_set_exec_mode(self._h, 1 if use_graph else 0))
 
     def prof_start(self):
         self._check(lib.bbot_prof_start(self._h))

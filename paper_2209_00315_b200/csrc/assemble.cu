@@ -353,6 +353,7 @@ void compute_residual(bbot_ctx* c, bool write_rhs) {
   for (double v : hs) tot += v;
   A.res_norm = std::sqrt(tot);
   A.scale = A.res_norm;      // ||(f;g;h)|| = ||F||
+  if (write_rhs) BB_CUDA(cudaMemcpyAsync(A.dscale.p, &A.scale, sizeof(double), cudaMemcpyHostToDevice, s));
 }
 
 // ---------------------------------------------------------------- T assembly

@@ -43,8 +43,8 @@ void copy_out(bbot_ctx* c, double* dst, const double* src, long long n, bbot_mem
 }
 void check_opts(const bbot_solver_opts& o) {
   BB_REQUIRE(o.eps_out > 0 && o.eps_T > 0 && o.eps_A > 0, BBOT_E_INPUT, "tolerances must be > 0");
-  BB_REQUIRE(o.restart >= 1 && o.restart <= 200 && o.maxit >= 1, BBOT_E_INPUT, "bad FGMRES restart/maxit");
-  BB_REQUIRE(o.restart_T >= 1 && o.restart_T <= 100 && o.maxit_inner >= 1, BBOT_E_INPUT, "bad inner caps");
+  BB_REQUIRE(o.restart >= 1 && o.restart <= GM_MAXR && o.maxit >= 1, BBOT_E_INPUT, "bad FGMRES restart/maxit");
+  BB_REQUIRE(o.restart_T >= 1 && o.restart_T <= GM_MAXR && o.maxit_inner >= 1, BBOT_E_INPUT, "bad inner caps");
   BB_REQUIRE(o.omega_A > 0 && o.omega_A < 2 && o.omega_T > 0 && o.omega_T < 2, BBOT_E_INPUT, "bad Jacobi weight");
   BB_REQUIRE(o.coarse_max_A >= 2 && o.coarse_max_A <= 120 && o.coarse_max_T >= 1 && o.coarse_max_T <= 8192,
              BBOT_E_INPUT, "bad coarse sizes");
@@ -96,7 +96,8 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
     int devid = 0;
     BB_CUDA(cudaGetDevice(&devid));
     BB_CUDA(cudaDeviceGetAttribute(&c->dev.num_sms, cudaDevAttrMultiProcessorCount, devid));
-    c->red.dev = &c->dev;
+    c->red.init(&c->dev, std::max(K + 2, 64));
+    if (const char* e = getenv("BBOT_EAGER")) c->use_graph = (atoi(e) == 0);
     for (int i = 0; i < nt; i++)
       BB_REQUIRE(rho_in[i] >= 0 && rho_f[i] >= 0 && std::isfinite(rho_in[i]) && std::isfinite(rho_f[i]),
                  BBOT_E_INPUT, "densities must be finite and >= 0");
@@ -119,6 +120,7 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
     c->tmp_m.alloc(m, s);
     c->tmp_m2.alloc(m, s);
     c->scal.alloc(8 * (size_t)(K + 2) + 64, s);
+    c->as.dscale.alloc(1, s);
     init_state(c, 1.0);
     sync(c->dev);
   } catch (const Error& e) {
@@ -134,6 +136,7 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
 void bbot_destroy(bbot_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->dev.stream);
+  drop_solve_graph(c);
   delete c;
 }
 
@@ -164,6 +167,7 @@ bbot_status bbot_set_opts(bbot_ctx* c, const bbot_solver_opts* o) {
   check_opts(*o);
   c->opts = *o;
   c->as.valid = false;
+  drop_solve_graph(c);
   API_END(c)
 }
 
@@ -253,14 +257,9 @@ bbot_status bbot_bb_apply(bbot_ctx* c, const double* r, double* z, bbot_mem mem,
   long long nm = c->n() + c->m();
   if (c->tmp_nm.n != (size_t)nm) { c->tmp_nm.alloc(nm, c->dev.stream); c->tmp_nm2.alloc(nm, c->dev.stream); }
   copy_in(c, c->tmp_nm.p, r, nm, mem);
-  c->bb_T_its = 0;
-  c->bb_A_max = 0;
-  c->bb_A_total = 0;
-  bb_apply(c, c->tmp_nm.p, c->tmp_nm2.p);
+  bb_apply(c, c->tmp_nm.p, c->tmp_nm2.p, inner_T_its, inner_A_its_max);
   copy_out(c, z, c->tmp_nm2.p, nm, mem);
   sync(c->dev);
-  if (inner_T_its) *inner_T_its = c->bb_T_its;
-  if (inner_A_its_max) *inner_A_its_max = c->bb_A_max;
   API_END(c)
 }
 
@@ -273,14 +272,7 @@ bbot_status bbot_solve(bbot_ctx* c, double* dphi, double* drho, double* ds, bbot
   copy_out(c, dphi, c->dphi.p, c->n(), mem);
   copy_out(c, drho, c->drho.p, c->m(), mem);
   copy_out(c, ds, c->ds.p, c->m(), mem);
-  if (st) {
-    // keep assembly timings if the caller passed them in
-    loc.t_assemble_ms = st->t_assemble_ms;
-    loc.t_setup_ms = st->t_setup_ms;
-    loc.amg_levels_A = (int)c->amgA.lv.size();
-    loc.amg_levels_T = (int)c->amgT.lv.size();
-    *st = loc;
-  }
+  if (st) *st = loc;
   API_END(c)
 }
 
@@ -323,11 +315,8 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
     for (int it = 0; it < o.newton_max; it++) {
       bbot_ipm_record rec;
       memset(&rec, 0, sizeof(rec));
-      assemble_all(c, &rec.solve);
-      double ta = rec.solve.t_assemble_ms, ts = rec.solve.t_setup_ms;
+      assemble_all(c, nullptr);
       solve(c, &rec.solve);
-      rec.solve.t_assemble_ms = ta;
-      rec.solve.t_setup_ms = ts;
       rec.alpha = newton_update(c, o.frac_to_boundary);
       c->have_dir = false;
       compute_residual(c, false);
@@ -429,6 +418,14 @@ bbot_status bbot_amg_vcycle(bbot_ctx* c, int which, const double* b, double* x, 
 }
 
 long long bbot_launch_count(const bbot_ctx* c) { return c ? c->dev.launches : 0; }
+
+bbot_status bbot_set_exec_mode(bbot_ctx* c, int use_graph) {
+  if (!c) return BBOT_E_INPUT;
+  API_BEGIN(c)
+  c->use_graph = use_graph != 0;
+  drop_solve_graph(c);
+  API_END(c)
+}
 
 bbot_status bbot_prof_start(bbot_ctx* c) {
   if (!c) return BBOT_E_INPUT;

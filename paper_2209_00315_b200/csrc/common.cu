@@ -3,12 +3,15 @@
 
 namespace bbot {
 
-__global__ void k_slice_final(const double* partial, int parts, double* out, int op_sqrt) {
-  int k = blockIdx.x;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < parts; i += blockDim.x) acc += partial[(size_t)k * parts + i];
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) out[k] = op_sqrt ? sqrt(acc) : acc;
+__global__ void k_cond_from_flag(LoopCtl L) { cudaGraphSetConditional(L.h, *L.flag ? 1u : 0u); }
+
+cudaStream_t capture_stream(Dev& d, int depth) {
+  while ((int)d.cap_streams.size() <= depth) {
+    cudaStream_t st;
+    BB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    d.cap_streams.push_back(st);
+  }
+  return d.cap_streams[depth];
 }
 
 __global__ void k_slice_final_min(const double* partial, int parts, double* out) {

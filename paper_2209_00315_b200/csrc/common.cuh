@@ -48,6 +48,9 @@ struct Dev {
   long long launches = 0;
   int num_sms = 148;
   bool prof = false;
+  bool capturing = false;      // kernels are being captured into a CUDA graph
+  int depth = 0;               // nesting depth of device loops being captured
+  std::vector<cudaStream_t> cap_streams;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get_event() {
@@ -61,6 +64,7 @@ struct Dev {
     return e;
   }
   ~Dev() {
+    for (auto st : cap_streams) cudaStreamDestroy(st);
     for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : pool) cudaEventDestroy(e);
   }
@@ -69,7 +73,7 @@ struct Dev {
 template <class K, class... Args>
 inline void launch(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, Args... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
-  if (d.prof) {
+  if (d.prof && !d.capturing) {
     ProfRec r{(const void*)kernel, d.get_event(), d.get_event()};
     cudaEventRecord(r.a, d.stream);
     kernel<<<grid, block, smem, d.stream>>>(args...);
@@ -78,7 +82,7 @@ inline void launch(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, Args...
   } else {
     kernel<<<grid, block, smem, d.stream>>>(args...);
   }
-  d.launches++;
+  if (!d.capturing) d.launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw Error(BBOT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -173,21 +177,92 @@ __device__ __forceinline__ double block_min(double v) {
   return v;
 }
 
-// Sliced reduction: out[k] = sum_{i < len} f(k, i) for k < nslices.
-// Phase 1: grid (parts, nslices), each block sums a fixed contiguous chunk.
-template <class F>
-__global__ void k_slice_partial(F f, long long len, int parts, double* partial) {
-  int k = blockIdx.y;
+// ---------------------------------------------------------------------------
+// Deterministic single-launch reductions ("last block finishes").
+//
+// Grid (parts, ns): block (p, k) reduces a fixed contiguous chunk of slice k and
+// writes its partial to partial[k*parts + p]; the block that arrives last at the
+// counter sums every slice's partials in a fixed order (warp per slice, lanes
+// strided, shuffle tree) into out[k] and then runs the caller's epilogue.  The
+// result depends only on (len, ns, parts), never on block scheduling, so it is
+// bitwise reproducible, and the scalar logic that consumes it (Givens rotations,
+// PCG alpha/beta, loop conditions) runs in the same launch.  One counter per
+// Reducer: launches on one stream are serialised, and the last block re-arms it.
+struct RedArgs {
+  double* partial;
+  unsigned* counter;
+  double* out;
+  int parts;
+};
+
+// Called by all threads of every block after the block's partial(s) are written
+// by thread 0.  Returns true in all threads of the last block.
+__device__ __forceinline__ bool red_last_block(unsigned* counter) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned total = gridDim.x * gridDim.y;
+    unsigned t = atomicAdd(counter, 1u);
+    s_last = (t == total - 1) ? 1 : 0;
+    if (s_last) {
+      __threadfence();
+      *counter = 0u;
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+// Last block only: out[s] = sum_p partial[s*parts + p], s < ns.  Ends with a barrier.
+__device__ __forceinline__ void red_finish(const double* partial, int parts, int ns, double* out) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int s = w; s < ns; s += nw) {
+    double v = 0.0;
+    for (int p = lane; p < parts; p += 32) v += __ldcg(partial + (size_t)s * parts + p);
+    v = warp_sum(v);
+    if (lane == 0) out[s] = v;
+  }
+  __syncthreads();
+}
+
+// Block (p, k) of a (parts, ns) grid: reduce acc and commit; last block finishes.
+__device__ __forceinline__ bool red_commit(double acc, const RedArgs& R) {
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) R.partial[(size_t)blockIdx.y * R.parts + blockIdx.x] = acc;
+  if (!red_last_block(R.counter)) return false;
+  red_finish(R.partial, R.parts, gridDim.y, R.out);
+  return true;
+}
+
+// chunk of slice-local indices owned by block p
+__device__ __forceinline__ void red_chunk(long long len, int parts, long long& beg, long long& end) {
   long long chunk = (len + parts - 1) / parts;
-  long long beg = (long long)blockIdx.x * chunk;
-  long long end = beg + chunk < len ? beg + chunk : len;
+  beg = (long long)blockIdx.x * chunk;
+  end = beg + chunk < len ? beg + chunk : len;
+}
+
+struct NoFin {
+  __device__ void operator()(const double*) const {}
+};
+struct SqrtFin {   // out[k] = sqrt(out[k])
+  double* out;
+  int ns;
+  __device__ void operator()(const double*) const {
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) out[k] = sqrt(out[k]);
+  }
+};
+
+// out[k] = sum_{i < len} f(k, i); then fin(out) in the last block (all threads).
+template <class F, class Fin>
+__global__ void k_slice_reduce(F f, long long len, RedArgs R, Fin fin) {
+  int k = blockIdx.y;
+  long long beg, end;
+  red_chunk(len, R.parts, beg, end);
   double acc = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) acc += f(k, i);
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) partial[(size_t)k * parts + blockIdx.x] = acc;
+  if (red_commit(acc, R)) fin(R.out);
 }
-// Phase 2: one block per slice, fixed-order tree over the partials.
-__global__ void k_slice_final(const double* partial, int parts, double* out, int op_sqrt);
 
 template <class F>
 __global__ void k_slice_partial_min(F f, long long len, int parts, double* partial) {
@@ -202,40 +277,135 @@ __global__ void k_slice_partial_min(F f, long long len, int parts, double* parti
 }
 __global__ void k_slice_final_min(const double* partial, int parts, double* out);
 
-// Workspace for reductions (partials), owned by the context.
+// Reduction workspace, owned by the context.  Sized once at creation (nothing is
+// allocated while a CUDA graph is being captured).
 struct Reducer {
   Dev* dev = nullptr;
   DBuf<double> partial;
+  DBuf<unsigned> counter;
+  size_t cap = 0;
+  static constexpr int BS = 256;
+  void init(Dev* d, int max_slices) {
+    dev = d;
+    cap = (size_t)8 * d->num_sms + 2 * (size_t)max_slices + 4096;
+    partial.alloc(cap, d->stream);
+    counter.alloc(1, d->stream);
+    counter.zero();
+  }
+  // blocks per slice: ~2048 elements per block, <= 8 blocks per SM in total
   int parts_for(long long len, int nslices) const {
     long long p = (len + 2047) / 2048;
-    long long cap = std::max(1LL, (long long)(4 * dev->num_sms) / std::max(1, nslices));
-    if (cap < 1) cap = 1;
-    p = std::min(p, std::max(1LL, cap));
+    long long cap_b = std::max(1LL, (long long)(8 * dev->num_sms) / std::max(1, nslices));
+    p = std::min(p, cap_b);
     p = std::min(p, 1024LL);
     return (int)std::max(1LL, p);
   }
-  void ensure(size_t n) { if (partial.n < n) partial.alloc(std::max(n, (size_t)4096), dev->stream); }
-
+  RedArgs args(int parts, int nslices, double* out) {
+    if ((size_t)parts * nslices > cap) throw Error(BBOT_E_INTERNAL, "reduction workspace too small");
+    return RedArgs{partial.p, counter.p, out, parts};
+  }
+  template <class F, class Fin>
+  void reduce(F f, long long len, int nslices, double* out, Fin fin) {
+    int parts = parts_for(len, nslices);
+    launch(*dev, k_slice_reduce<F, Fin>, dim3(parts, nslices), dim3(BS), 0, f, len, args(parts, nslices, out), fin);
+  }
   template <class F>
   void slice_sum(F f, long long len, int nslices, double* out, bool take_sqrt = false) {
-    int parts = parts_for(len, nslices);
-    ensure((size_t)parts * nslices);
-    launch(*dev, k_slice_partial<F>, dim3(parts, nslices), dim3(256), 0, f, len, parts, partial.p);
-    launch(*dev, k_slice_final, dim3(nslices), dim3(256), 0, (const double*)partial.p, parts, out,
-           (int)take_sqrt);
+    if (take_sqrt) reduce(f, len, nslices, out, SqrtFin{out, nslices});
+    else reduce(f, len, nslices, out, NoFin{});
   }
   template <class F>
   void slice_min(F f, long long len, int nslices, double* out) {
     int parts = parts_for(len, nslices);
-    ensure((size_t)parts * nslices);
-    launch(*dev, k_slice_partial_min<F>, dim3(parts, nslices), dim3(256), 0, f, len, parts, partial.p);
-    launch(*dev, k_slice_final_min, dim3(nslices), dim3(256), 0, (const double*)partial.p, parts, out);
+    args(parts, nslices, out);
+    launch(*dev, k_slice_partial_min<F>, dim3(parts, nslices), dim3(BS), 0, f, len, parts, partial.p);
+    launch(*dev, k_slice_final_min, dim3(nslices), dim3(BS), 0, (const double*)partial.p, parts, out);
   }
 };
+
+// ---------------------------------------------------------------------------
+// Device-controlled loops.  The loop condition lives in device memory (`flag`)
+// and is written by the body's last control kernel.  Under graph capture a loop
+// becomes a conditional WHILE node whose handle the control kernel also sets
+// (cudaGraphSetConditional), so a whole Krylov solve -- nested loops included --
+// is one graph launch with no host round trip.  Eagerly (profiling, debugging,
+// single calls) the same body runs on the stream and the host reads the flag.
+struct LoopCtl {
+  cudaGraphConditionalHandle h;
+  int* flag;
+  int graph;
+  __device__ __forceinline__ void set(int v) const {
+    *flag = v;
+    if (graph) cudaGraphSetConditional(h, v ? 1u : 0u);
+  }
+};
+
+__global__ void k_cond_from_flag(LoopCtl L);
+
+cudaStream_t capture_stream(Dev& d, int depth);
+
+template <class Body>
+void dev_while(Dev& d, int* flag, Body&& body) {
+  if (!d.capturing) {
+    LoopCtl L{0, flag, 0};
+    d.launches++;            // the graph's k_cond_from_flag, so eager and graph counts agree
+    while (true) {
+      int f = 0;
+      BB_CUDA(cudaMemcpyAsync(&f, flag, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
+      BB_CUDA(cudaStreamSynchronize(d.stream));
+      if (!f) break;
+      body(L);
+    }
+    return;
+  }
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  BB_CUDA(cudaStreamGetCaptureInfo(d.stream, &st, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  BB_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  LoopCtl L{h, flag, 1};
+  launch(d, k_cond_from_flag, dim3(1), dim3(1), 0, L);
+  BB_CUDA(cudaStreamGetCaptureInfo(d.stream, &st, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  BB_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  cudaGraph_t body_g = p.conditional.phGraph_out[0];
+  BB_CUDA(cudaStreamUpdateCaptureDependencies(d.stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t outer = d.stream;
+  cudaStream_t inner = capture_stream(d, ++d.depth);
+  BB_CUDA(cudaStreamBeginCaptureToGraph(inner, body_g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  d.stream = inner;
+  try {
+    body(L);
+  } catch (...) {
+    d.stream = outer;
+    d.depth--;
+    cudaGraph_t junk;
+    cudaStreamEndCapture(inner, &junk);
+    throw;
+  }
+  d.stream = outer;
+  d.depth--;
+  BB_CUDA(cudaStreamEndCapture(inner, nullptr));
+}
 
 // Exclusive scan of int64 (len n) -> out (len n+1, out[n] = total).  In-place safe.
 void exclusive_scan(Dev& d, const long long* in, long long* out, long long n, DBuf<long long>& ws);
 void exclusive_scan_i32(Dev& d, const int* in, long long* out, long long n, DBuf<long long>& ws);
+
+// address of a member of a device-resident struct (no dereference on the host)
+template <class S, class T>
+inline T* dev_field(S* base, T S::*m) {
+  static const S probe{};
+  size_t off = (size_t)(reinterpret_cast<const char*>(&(probe.*m)) - reinterpret_cast<const char*>(&probe));
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
+}
 
 // Host helpers
 inline void sync(Dev& d) { BB_CUDA(cudaStreamSynchronize(d.stream)); }

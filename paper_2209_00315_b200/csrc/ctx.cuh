@@ -60,6 +60,7 @@ struct Assembled {
   DBuf<double> rhs;               // (f; P gt)  (n+m)
   DBuf<double> Tv;                // [K][3][W][nbar]
   double scale = 0;               // ||(f;g;h)||
+  DBuf<double> dscale;            // the same on the device (read by the captured solve)
   double res_norm = 0;            // ||F||
 };
 
@@ -84,14 +85,18 @@ struct bbot_ctx {
   bool have_dir = false;
   bbot::DBuf<double> sol, dphi, drho, ds;
   // workspaces
-  bbot::Fgmres outer, innerT;
-  bbot::PcgSlices pcg;
+  bbot::DevGmres outer, innerT;
+  bbot::DevPcg pcg;
+  // CUDA graph of one whole solve (FGMRES + BB applies + recovery), captured
+  // after each assembly (the AMG hierarchies it reads are rebuilt per step)
+  bool use_graph = true;
+  cudaGraphExec_t solve_exec = nullptr;
+  double t_capture_ms = 0;      // last capture + instantiate (0 when the graph was replayed)
+  double t_assemble_ms = 0, t_setup_ms = 0;   // last bbot_assemble
   bbot::DBuf<double> tmp_n, tmp_n2, tmp_m, tmp_m2, tmp_nm, tmp_nm2;
   bbot::DBuf<double> scal;      // device scalars / per-slice scratch (>= 8*(K+2))
   bbot::DBuf<long long> scan_ws;
-  // counters for the current solve
-  int bb_T_its = 0, bb_A_max = 0;
-  long long bb_A_total = 0;
+  bbot::DBuf<double> nrm_T;      // ||r2|| of the current BB apply (device scalar)
   long long n() const { return (long long)g.N * (g.K + 1); }
   long long m() const { return (long long)g.nbar * g.K; }
 };

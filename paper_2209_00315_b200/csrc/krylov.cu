@@ -1,4 +1,6 @@
-// krylov.cu -- FGMRES(restart) with CGS2 and per-slice PCG (see krylov.cuh).
+// krylov.cu -- device-resident FGMRES(restart) with CGS2 and per-slice PCG
+// (see krylov.cuh).  Every scalar decision is taken on the device by the last
+// block of a fused reduction; the host only emits kernels and loops.
 #include "krylov.cuh"
 #include <cmath>
 
@@ -16,46 +18,22 @@ __global__ void k_scale(const double* __restrict__ a, double s, double* __restri
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = s * a[i];
 }
-__global__ void k_scale_inv_dev(const double* __restrict__ a, const double* __restrict__ s, double* __restrict__ b,
-                                long long n) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  double v = *s;
-  if (i < n) b[i] = v > TINY ? a[i] / v : 0.0;
-}
 __global__ void k_axpby(double alpha, const double* __restrict__ a, double beta, double* __restrict__ b, long long n) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = alpha * a[i] + beta * b[i];
 }
-__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c, long long n) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) c[i] = a[i] - b[i];
-}
-// w[i] += sign * sum_k h[k] V[k][i]
-__global__ void k_multi_axpy(double* __restrict__ w, const double* __restrict__ V, const double* __restrict__ h,
-                             int cnt, long long n, double sign) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__global__ void k_neg_norm(long long n, const double* __restrict__ a, double* __restrict__ b, RedArgs R,
+                           double* norm) {
+  long long beg, end;
+  red_chunk(n, R.parts, beg, end);
   double acc = 0.0;
-  for (int k = 0; k < cnt; k++) acc += h[k] * V[(size_t)k * n + i];
-  w[i] += sign * acc;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = a[i];
+    b[i] = -v;
+    acc += v * v;
+  }
+  if (red_commit(acc, R) && threadIdx.x == 0) *norm = sqrt(R.out[0]);
 }
-
-struct DotVW {
-  const double* V;
-  const double* w;
-  long long n;
-  __device__ double operator()(int k, long long i) const { return V[(size_t)k * n + i] * w[i]; }
-};
-struct Sq {
-  const double* a;
-  __device__ double operator()(int, long long i) const { return a[i] * a[i]; }
-};
-struct SliceDot {
-  const double* a;
-  const double* b;
-  long long L;
-  __device__ double operator()(int k, long long i) const { return a[(size_t)k * L + i] * b[(size_t)k * L + i]; }
-};
 
 void dev_copy(Dev& d, const double* a, double* b, long long n) {
   launch(d, k_copy, dim3(nblocks(n, BS)), dim3(BS), 0, a, b, n);
@@ -66,211 +44,357 @@ void dev_scale(Dev& d, const double* a, double s, double* b, long long n) {
 void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, long long n) {
   launch(d, k_axpby, dim3(nblocks(n, BS)), dim3(BS), 0, alpha, a, beta, b, n);
 }
-double dev_norm(Dev& d, Reducer& red, const double* a, long long n, double* dscratch) {
-  red.slice_sum(Sq{a}, n, 1, dscratch, true);
-  return read_scalar(d, dscratch);
+void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n, double* norm) {
+  int parts = red.parts_for(n, 1);
+  launch(d, k_neg_norm, dim3(parts), dim3(BS), 0, n, a, b, red.args(parts, 1, norm), norm);
 }
 
-// ------------------------------------------------------------ FGMRES
-void Fgmres::ensure(Dev& d, long long n_, int restart_) {
+// ------------------------------------------------------------ FGMRES kernels
+// All take the device scalar block G.  Vectors have length n; V is [(r+1)][n].
+
+__global__ void k_gm_init(GmresScal* G, const double* scale, double tol, int maxit, int restart) {
+  G->its = 0;
+  G->conv = 0;
+  G->brk = 0;
+  G->maxit = maxit;
+  G->restart = restart;
+  G->scale = *scale;
+  G->target = tol * G->scale;
+  G->res = 0.0;
+  G->jj = 0;
+  G->flag_outer = 1;
+  G->flag_inner = 0;
+}
+
+// w = b - w (w = op(x) on entry);  beta = ||w||; start a cycle or stop
+__global__ void k_gm_residual(long long n, const double* __restrict__ b, double* __restrict__ w, GmresScal* G,
+                              RedArgs R) {
+  long long beg, end;
+  red_chunk(n, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = b[i] - w[i];
+    w[i] = v;
+    acc += v * v;
+  }
+  if (red_commit(acc, R) && threadIdx.x == 0) {
+    double beta = sqrt(R.out[0]);
+    G->beta = beta;
+    G->res = beta;
+    G->j = 0;
+    G->jj = 0;
+    if (!(beta > G->target)) {
+      G->conv = 1;
+      G->flag_inner = 0;
+    } else {
+      G->flag_inner = 1;
+      for (int i = 0; i <= GM_MAXR; i++) G->g[i] = 0.0;
+      G->g[0] = beta;
+    }
+  }
+}
+
+// V[j] = w / s and vin = V[j], s = beta (start) or hn (Arnoldi), only if the inner loop continues
+__global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __restrict__ V,
+                           double* __restrict__ vin, const GmresScal* G, int start) {
+  if (!G->flag_inner) return;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = start ? G->beta : G->hn;
+  int j = start ? 0 : G->j;
+  double v = w[i] / s;
+  V[(size_t)j * n + i] = v;
+  vin[i] = v;
+}
+
+// h[k] = V[k] . w for k <= j (one pass over w, one register accumulator per k);
+// optionally copy zout -> Z[j] in the same pass
+template <bool COPYZ>
+__global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __restrict__ V,
+                                                 const double* __restrict__ w, const double* __restrict__ zout,
+                                                 double* __restrict__ Z, GmresScal* G, int which, RedArgs R) {
+  const int j = G->j;
+  long long beg, end;
+  red_chunk(n, R.parts, beg, end);
+  double acc[GM_MAXR];
+#pragma unroll
+  for (int k = 0; k < GM_MAXR; k++) acc[k] = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double wi = w[i];
+    if (COPYZ) Z[(size_t)j * n + i] = zout[i];
+#pragma unroll
+    for (int k = 0; k < GM_MAXR; k++)
+      if (k <= j) acc[k] += V[(size_t)k * n + i] * wi;
+  }
+#pragma unroll
+  for (int k = 0; k < GM_MAXR; k++) {
+    if (k <= j) {
+      double s = block_sum(acc[k]);
+      if (threadIdx.x == 0) R.partial[(size_t)k * R.parts + blockIdx.x] = s;
+    }
+  }
+  if (!red_last_block(R.counter)) return;
+  double* out = which == 0 ? G->h1 : G->h2;
+  red_finish(R.partial, R.parts, j + 1, out);
+}
+
+// w -= sum_{k<=j} h[k] V[k]  (h = h1 or h2); with GIVENS: partial ||w||^2 and,
+// in the last block, the Hessenberg column, Givens rotations, residual estimate
+// and the inner-loop decision (Saad's FGMRES).
+template <bool GIVENS>
+__global__ void __launch_bounds__(256) k_gm_orth(long long n, const double* __restrict__ V, double* __restrict__ w,
+                                                 GmresScal* G, int which, RedArgs R, LoopCtl inner) {
+  const int j = G->j;
+  const double* h = which == 0 ? G->h1 : G->h2;
+  __shared__ double hs[GM_MAXR + 1];
+  if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  long long beg, end;
+  red_chunk(n, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k <= j; k++) s += hs[k] * V[(size_t)k * n + i];
+    double v = w[i] - s;
+    w[i] = v;
+    acc += v * v;
+  }
+  if (!GIVENS) return;
+  if (!red_commit(acc, R) || threadIdx.x != 0) return;
+  const int r = G->restart;
+  double hn = sqrt(R.out[0]);
+  double* H = G->H;
+  for (int i = 0; i <= j; i++) H[i * GM_MAXR + j] = G->h1[i] + G->h2[i];
+  H[(j + 1) * GM_MAXR + j] = hn;
+  for (int i = 0; i < j; i++) {
+    double t = G->cs[i] * H[i * GM_MAXR + j] + G->sn[i] * H[(i + 1) * GM_MAXR + j];
+    H[(i + 1) * GM_MAXR + j] = -G->sn[i] * H[i * GM_MAXR + j] + G->cs[i] * H[(i + 1) * GM_MAXR + j];
+    H[i * GM_MAXR + j] = t;
+  }
+  double den = hypot(H[j * GM_MAXR + j], H[(j + 1) * GM_MAXR + j]);
+  G->cs[j] = H[j * GM_MAXR + j] / den;
+  G->sn[j] = H[(j + 1) * GM_MAXR + j] / den;
+  H[j * GM_MAXR + j] = den;
+  H[(j + 1) * GM_MAXR + j] = 0.0;
+  G->g[j + 1] = -G->sn[j] * G->g[j];
+  G->g[j] = G->cs[j] * G->g[j];
+  double res = fabs(G->g[j + 1]);
+  G->res = res;
+  G->jj = j + 1;
+  G->its += 1;
+  G->total_its += 1;
+  G->hn = hn;
+  if (hn <= TINY) G->brk = 1;
+  int cont = !(res <= G->target || G->its >= G->maxit || G->brk) && (j + 1 < r);
+  G->j = j + 1;
+  G->flag_inner = cont;
+  inner.set(cont);
+}
+
+// x += Z y with y = H^{-1} g (back substitution, redundantly per block); block 0
+// also takes the restart decision for the outer loop.
+__global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __restrict__ Z, double* __restrict__ x,
+                                                   GmresScal* G, LoopCtl outer) {
+  __shared__ double y[GM_MAXR];
+  const int jj = G->jj;
+  if (threadIdx.x == 0) {
+    for (int i = jj - 1; i >= 0; i--) {
+      double acc = G->g[i];
+      for (int k = i + 1; k < jj; k++) acc -= G->H[i * GM_MAXR + k] * y[k];
+      y[i] = acc / G->H[i * GM_MAXR + i];
+    }
+  }
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < jj; k++) s += y[k] * Z[(size_t)k * n + i];
+    if (jj > 0) x[i] += s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (G->res <= G->target || G->brk) G->conv = 1;
+    int cont = !G->conv && G->its < G->maxit;
+    G->flag_outer = cont;
+    outer.set(cont);
+  }
+}
+
+__global__ void k_gm_reset_total(GmresScal* G) { G->total_its = 0; }
+
+void DevGmres::ensure(Dev& d, long long n_, int restart_) {
+  if (restart_ > GM_MAXR) throw Error(BBOT_E_INPUT, "restart > 32 not supported");
   if (n == n_ && restart == restart_ && V.p) return;
   n = n_;
   restart = restart_;
   V.alloc((size_t)(restart + 1) * n, d.stream);
   Z.alloc((size_t)restart * n, d.stream);
   w.alloc(n, d.stream);
-  hdev.alloc(2 * (restart + 2) + 2, d.stream);
-  ydev.alloc(restart + 1, d.stream);
-  if (hhost) cudaFreeHost(hhost);
-  hhost = nullptr;
-  BB_CUDA(cudaMallocHost((void**)&hhost, sizeof(double) * (2 * (restart_ + 2) + 8)));
-}
-Fgmres::~Fgmres() {
-  if (hhost) cudaFreeHost(hhost);
+  vin.alloc(n, d.stream);
+  zout.alloc(n, d.stream);
+  if (!sc.p) {
+    sc.alloc(1, d.stream);
+    BB_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(GmresScal), d.stream));
+  }
 }
 
-KrylovResult Fgmres::solve(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
-                           double scale, double tol, int maxit) {
-  KrylovResult R;
-  const double target = tol * scale;
-  unsigned nb = nblocks(n, BS);
+void DevGmres::reset_total(Dev& d) { launch(d, k_gm_reset_total, dim3(1), dim3(1), 0, sc.p); }
+
+void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
+                    const double* scale, double tol, int maxit) {
+  const int parts = red.parts_for(n, 1);
+  const unsigned nb = nblocks(n, BS);
+  const unsigned nb_upd = std::min<unsigned>(nb, 8u * d.num_sms);
+  GmresScal* G = sc.p;
+  double* rout = reinterpret_cast<double*>(dev_field(G, &GmresScal::red_out));
+  launch(d, k_gm_init, dim3(1), dim3(1), 0, G, scale, tol, maxit, restart);
   BB_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), d.stream));
-  double* hd = hdev.p;                      // [0..r]: h, [r+1..2r+1]: h2, [2r+2]: norm
-  const int r = restart;
-  // r0 = b
-  red.slice_sum(Sq{b}, n, 1, hd + 2 * r + 2, true);
-  double beta = read_scalar(d, hd + 2 * r + 2);
-  if (!(beta > target)) { R.converged = true; R.res = beta; return R; }
-  launch(d, k_scale, dim3(nb), dim3(BS), 0, b, 1.0 / beta, V.p, n);
-  std::vector<double> H((size_t)(r + 1) * r), cs(r), sn(r), g(r + 1), y(r);
-  double res = beta;
-  int its = 0;
-  bool conv = false;
-  while (true) {
-    std::fill(H.begin(), H.end(), 0.0);
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
-    int jj = 0;
-    bool breakdown = false;
-    for (int j = 0; j < r; j++) {
-      double* Vj = V.p + (size_t)j * n;
-      double* Zj = Z.p + (size_t)j * n;
-      pre(Vj, Zj);
-      op(Zj, w.p);
-      its++;
-      // CGS2
-      red.slice_sum(DotVW{V.p, w.p, n}, n, j + 1, hd, false);
-      launch(d, k_multi_axpy, dim3(nb), dim3(BS), 0, w.p, (const double*)V.p, (const double*)hd, j + 1, n, -1.0);
-      red.slice_sum(DotVW{V.p, w.p, n}, n, j + 1, hd + r + 1, false);
-      launch(d, k_multi_axpy, dim3(nb), dim3(BS), 0, w.p, (const double*)V.p, (const double*)(hd + r + 1), j + 1,
-             n, -1.0);
-      red.slice_sum(Sq{w.p}, n, 1, hd + 2 * r + 2, true);
-      launch(d, k_scale_inv_dev, dim3(nb), dim3(BS), 0, (const double*)w.p, (const double*)(hd + 2 * r + 2),
-             V.p + (size_t)(j + 1) * n, n);
-      BB_CUDA(cudaMemcpyAsync(hhost, hd, sizeof(double) * (2 * r + 3), cudaMemcpyDeviceToHost, d.stream));
-      sync(d);
-      double hn = hhost[2 * r + 2];
-      for (int i = 0; i <= j; i++) H[(size_t)i * r + j] = hhost[i] + hhost[r + 1 + i];
-      H[(size_t)(j + 1) * r + j] = hn;
-      for (int i = 0; i < j; i++) {
-        double t = cs[i] * H[(size_t)i * r + j] + sn[i] * H[(size_t)(i + 1) * r + j];
-        H[(size_t)(i + 1) * r + j] = -sn[i] * H[(size_t)i * r + j] + cs[i] * H[(size_t)(i + 1) * r + j];
-        H[(size_t)i * r + j] = t;
-      }
-      double den = std::hypot(H[(size_t)j * r + j], H[(size_t)(j + 1) * r + j]);
-      cs[j] = H[(size_t)j * r + j] / den;
-      sn[j] = H[(size_t)(j + 1) * r + j] / den;
-      H[(size_t)j * r + j] = den;
-      H[(size_t)(j + 1) * r + j] = 0.0;
-      g[j + 1] = -sn[j] * g[j];
-      g[j] = cs[j] * g[j];
-      res = std::fabs(g[j + 1]);
-      jj = j + 1;
-      if (hn <= TINY) breakdown = true;
-      if (res <= target || its >= maxit || breakdown) break;
-    }
-    for (int i = jj - 1; i >= 0; i--) {
-      double acc = g[i];
-      for (int k = i + 1; k < jj; k++) acc -= H[(size_t)i * r + k] * y[k];
-      y[i] = acc / H[(size_t)i * r + i];
-    }
-    BB_CUDA(cudaMemcpyAsync(ydev.p, y.data(), jj * sizeof(double), cudaMemcpyHostToDevice, d.stream));
-    launch(d, k_multi_axpy, dim3(nb), dim3(BS), 0, x, (const double*)Z.p, (const double*)ydev.p, jj, n, 1.0);
-    sync(d);  // y lives on the host stack
-    if (res <= target || breakdown) { conv = true; break; }
-    if (its >= maxit) break;
-    // restart with the true residual
-    op(x, w.p);
-    launch(d, k_sub, dim3(nb), dim3(BS), 0, b, (const double*)w.p, w.p, n);
-    red.slice_sum(Sq{w.p}, n, 1, hd + 2 * r + 2, true);
-    beta = read_scalar(d, hd + 2 * r + 2);
-    res = beta;
-    if (beta <= target) { conv = true; break; }
-    launch(d, k_scale, dim3(nb), dim3(BS), 0, (const double*)w.p, 1.0 / beta, V.p, n);
-  }
-  R.its = its;
-  R.converged = conv;
-  R.res = res;
-  return R;
+  dev_while(d, dev_field(G, &GmresScal::flag_outer), [&](const LoopCtl& outer) {
+    op(x, w.p);                                               // x = 0 in the first cycle: w = 0 exactly
+    launch(d, k_gm_residual, dim3(parts), dim3(BS), 0, n, b, w.p, G, red.args(parts, 1, rout));
+    launch(d, k_gm_scale, dim3(nb), dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 1);
+    dev_while(d, dev_field(G, &GmresScal::flag_inner), [&](const LoopCtl& inner) {
+      pre(vin.p, zout.p);
+      op(zout.p, w.p);
+      // CGS2: two classical Gram-Schmidt passes
+      launch(d, k_gm_dots<true>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+             (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
+      launch(d, k_gm_orth<false>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G, 0,
+             red.args(parts, 1, nullptr), inner);
+      launch(d, k_gm_dots<false>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+             (const double*)nullptr, (double*)nullptr, G, 1, red.args(parts, restart + 1, nullptr));
+      launch(d, k_gm_orth<true>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G, 1,
+             red.args(parts, 1, rout), inner);
+      launch(d, k_gm_scale, dim3(nb), dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0);
+    });
+    launch(d, k_gm_update, dim3(nb_upd), dim3(BS), 0, n, (const double*)Z.p, x, G, outer);
+  });
 }
 
 // ------------------------------------------------------------ per-slice PCG
-// sc layout: [0] bn [1] rn [2] rz [3] rzn [4] pq [5] alpha [6] beta [7] active, each nslices
-__global__ void k_pcg_init(int ns, double* sc, int* its) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= ns) return;
-  sc[7 * ns + k] = sc[0 * ns + k] > 0.0 ? 1.0 : 0.0;
-  sc[1 * ns + k] = sc[0 * ns + k];
-  its[k] = 0;
-}
-__global__ void k_pcg_alpha(int ns, double* sc, int* its) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= ns) return;
-  double act = sc[7 * ns + k];
-  double pq = sc[4 * ns + k];
-  if (act != 0.0 && !(pq > 0.0)) act = 0.0;
-  sc[7 * ns + k] = act;
-  sc[5 * ns + k] = act != 0.0 ? sc[2 * ns + k] / pq : 0.0;
-  its[k] += act != 0.0 ? 1 : 0;
-}
-__global__ void k_pcg_xr(long long L, int ns, const double* __restrict__ sc, double* __restrict__ x,
-                         double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ q) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L * ns) return;
-  double a = sc[5 * ns + i / L];
-  x[i] += a * p[i];
-  r[i] -= a * q[i];
-}
-__global__ void k_pcg_check(int ns, double* sc, double tol, int* any) {
-  // single block
-  int cnt = 0;
-  for (int k = threadIdx.x; k < ns; k += blockDim.x) {
-    double act = sc[7 * ns + k];
-    if (act != 0.0 && !(sc[1 * ns + k] > tol * sc[0 * ns + k])) act = 0.0;
-    sc[7 * ns + k] = act;
-    cnt += act != 0.0;
+__global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,
+                            PcgScal* P, int maxit, RedArgs R) {
+  int k = blockIdx.y;
+  const int ns = gridDim.y;
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = b[(size_t)k * L + i];
+    r[(size_t)k * L + i] = v;
+    acc += v * v;
   }
-  cnt = __syncthreads_count(cnt > 0);
-  if (threadIdx.x == 0) *any = cnt;
-}
-__global__ void k_pcg_beta(int ns, double* sc) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= ns) return;
-  double act = sc[7 * ns + k];
-  double rz = sc[2 * ns + k], rzn = sc[3 * ns + k];
-  sc[6 * ns + k] = act != 0.0 ? rzn / (rz != 0.0 ? rz : 1.0) : 0.0;
-  if (act != 0.0) sc[2 * ns + k] = rzn;
-}
-__global__ void k_pcg_p(long long L, int ns, const double* __restrict__ sc, const double* __restrict__ z,
-                        double* __restrict__ p) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L * ns) return;
-  p[i] = z[i] + sc[6 * ns + i / L] * p[i];
+  if (!red_commit(acc, R)) return;
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+    double bn = sqrt(R.out[q]);
+    s[PS_BN * ns + q] = bn;
+    s[PS_RN * ns + q] = bn;
+    s[PS_ACTIVE * ns + q] = bn > 0.0 ? 1.0 : 0.0;
+    s[PS_BETA * ns + q] = 0.0;
+    its[q] = 0;
+    if (bn > 0.0) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    P->it = 0;
+    P->maxit = maxit;
+    P->flag = (any && maxit > 0) ? 1 : 0;
+  }
 }
 
-std::vector<int> PcgSlices::solve(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b,
-                                  double* x, int ns, long long L, double tol, int maxit) {
-  long long N = L * ns;
-  cudaStream_t s = d.stream;
-  if (n != N) {
-    n = N;
-    r.alloc(N, s); z.alloc(N, s); p.alloc(N, s); q.alloc(N, s);
+__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, double* s,
+                         const PcgScal* P, RedArgs R) {
+  int k = blockIdx.y;
+  const int ns = gridDim.y;
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) acc += r[(size_t)k * L + i] * z[(size_t)k * L + i];
+  if (!red_commit(acc, R)) return;
+  const int it = P->it;
+  for (int q = threadIdx.x; q < ns; q += blockDim.x) {
+    double rzn = R.out[q];
+    if (it == 0) {
+      s[PS_RZ * ns + q] = rzn;
+      s[PS_BETA * ns + q] = 0.0;
+    } else {
+      double act = s[PS_ACTIVE * ns + q];
+      double rz = s[PS_RZ * ns + q];
+      s[PS_BETA * ns + q] = act != 0.0 ? rzn / (rz != 0.0 ? rz : 1.0) : 0.0;
+      if (act != 0.0) s[PS_RZ * ns + q] = rzn;
+    }
   }
-  if (nslices != ns || !sc.p) {
-    nslices = ns;
-    sc.alloc(8 * (size_t)ns, s);
-    its.alloc(ns, s);
-    any.alloc(1, s);
-  }
-  unsigned nb = nblocks(N, BS), nbs = nblocks(ns, 128);
-  double* S = sc.p;
-  BB_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double), s));
-  dev_copy(d, b, r.p, N);
-  red.slice_sum(SliceDot{b, b, L}, L, ns, S + 0 * ns, true);
-  launch(d, k_pcg_init, dim3(nbs), dim3(128), 0, ns, S, its.p);
-  launch(d, k_pcg_check, dim3(1), dim3(1024), 0, ns, S, -1.0, any.p);  // any active?
-  std::vector<int> out(ns, 0);
-  if (read_scalar(d, any.p) == 0) return out;
-  pre(r.p, z.p);
-  dev_copy(d, z.p, p.p, N);
-  red.slice_sum(SliceDot{r.p, z.p, L}, L, ns, S + 2 * ns, false);
-  for (int it = 0; it < maxit; it++) {
-    op(p.p, q.p);
-    red.slice_sum(SliceDot{p.p, q.p, L}, L, ns, S + 4 * ns, false);
-    launch(d, k_pcg_alpha, dim3(nbs), dim3(128), 0, ns, S, its.p);
-    launch(d, k_pcg_xr, dim3(nb), dim3(BS), 0, L, ns, (const double*)S, x, r.p, (const double*)p.p,
-           (const double*)q.p);
-    red.slice_sum(SliceDot{r.p, r.p, L}, L, ns, S + 1 * ns, true);
-    launch(d, k_pcg_check, dim3(1), dim3(1024), 0, ns, S, tol, any.p);
-    if (read_scalar(d, any.p) == 0) break;
-    pre(r.p, z.p);
-    red.slice_sum(SliceDot{r.p, z.p, L}, L, ns, S + 3 * ns, false);
-    launch(d, k_pcg_beta, dim3(nbs), dim3(128), 0, ns, S);
-    launch(d, k_pcg_p, dim3(nb), dim3(BS), 0, L, ns, (const double*)S, (const double*)z.p, p.p);
-  }
-  BB_CUDA(cudaMemcpyAsync(out.data(), its.p, ns * sizeof(int), cudaMemcpyDeviceToHost, s));
-  sync(d);
-  return out;
 }
+
+__global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ q, double* s, const int* its, PcgScal* P, double tol, RedArgs R,
+                         LoopCtl ctl) {
+  int k = blockIdx.y;
+  const int ns = gridDim.y;
+  const double a = s[PS_ALPHA * ns + k];
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    size_t t = (size_t)k * L + i;
+    x[t] += a * p[t];
+    double rv = r[t] - a * q[t];
+    r[t] = rv;
+    acc += rv * rv;
+  }
+  if (!red_commit(acc, R)) return;
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int w = threadIdx.x; w < ns; w += blockDim.x) {
+    double rn = sqrt(R.out[w]);
+    s[PS_RN * ns + w] = rn;
+    double act = s[PS_ACTIVE * ns + w];
+    if (act != 0.0 && !(rn > tol * s[PS_BN * ns + w])) act = 0.0;
+    s[PS_ACTIVE * ns + w] = act;
+    if (act != 0.0) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int it = P->it + 1;
+    P->it = it;
+    int cont = any && it < P->maxit;
+    if (!cont) {
+      int mx = 0;
+      long long tot = 0;
+      for (int w = 0; w < ns; w++) {
+        mx = max(mx, its[w]);
+        tot += its[w];
+      }
+      P->A_max = max(P->A_max, mx);
+      P->A_total += tot;
+    }
+    ctl.set(cont);
+  }
+}
+
+__global__ void k_pcg_reset(PcgScal* P) {
+  P->A_max = 0;
+  P->A_total = 0;
+}
+
+void DevPcg::ensure(Dev& d, long long n_, int ns_) {
+  if (n == n_ && nslices == ns_ && r.p) return;
+  n = n_;
+  nslices = ns_;
+  r.alloc(n, d.stream);
+  z.alloc(n, d.stream);
+  p.alloc(n, d.stream);
+  q.alloc(n, d.stream);
+  s.alloc((size_t)PS_COUNT * ns_, d.stream);
+  its.alloc(ns_, d.stream);
+  if (!sc.p) {
+    sc.alloc(1, d.stream);
+    BB_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(PcgScal), d.stream));
+  }
+}
+
+void DevPcg::reset_stats(Dev& d) { launch(d, k_pcg_reset, dim3(1), dim3(1), 0, sc.p); }
 
 }  // namespace bbot

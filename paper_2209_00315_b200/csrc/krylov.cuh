@@ -1,8 +1,16 @@
 // krylov.cuh -- I1/I5: right-preconditioned flexible GMRES(restart) with CGS2
-// ([Saad 1993]; cap P:1770) and I4: per-time-slice PCG
-// (P:1469).  Host control, device work: all vector arithmetic in kernels with
-// deterministic reductions; the (restart+1) x restart Hessenberg and its Givens
-// rotations live on the host (a few hundred flops per iteration).
+// ("applied as right preconditioners within a FGMRES cycle",
+// [Saad 1993]; cap P:1770) and I4: per-time-slice PCG.
+//
+// Device-resident: the Hessenberg matrix, Givens rotations, residual estimate,
+// per-slice PCG scalars, iteration counters and loop conditions all live in
+// device memory and are updated by the last block of the fused reduction that
+// produces them (common.cuh).  The host only *issues* work: each solver is a
+// capture function that emits kernels and device loops (dev_while), so a whole
+// nested solve can be recorded once into a CUDA graph with conditional WHILE
+// nodes and replayed with no host round trip, or run eagerly (host reads the
+// loop flags) for per-launch profiling.  Both modes run the same kernels on the
+// same data and give bitwise-identical results.
 #pragma once
 #include "common.cuh"
 #include <functional>
@@ -11,40 +19,144 @@ namespace bbot {
 
 using DevOp = std::function<void(const double*, double*)>;
 
-struct KrylovResult {
-  int its = 0;
-  bool converged = false;
-  double res = 0;
+constexpr int GM_MAXR = 32;   // max restart length (CGS2 dot kernel keeps one accumulator per basis vector)
+
+// device scalar block of one GMRES instance
+struct GmresScal {
+  double H[(GM_MAXR + 1) * GM_MAXR];   // row-major (GM_MAXR+1) x GM_MAXR
+  double cs[GM_MAXR], sn[GM_MAXR], g[GM_MAXR + 1];
+  double h1[GM_MAXR + 1], h2[GM_MAXR + 1];
+  double beta, res, target, hn, scale;
+  double red_out[4];                    // reduction results consumed by the epilogues
+  int j, its, jj, conv, brk, maxit, restart;
+  int flag_outer, flag_inner;
+  long long total_its;                  // accumulated over a whole Newton solve (inner T statistic)
 };
 
-struct Fgmres {
+struct DevGmres {
   long long n = 0;
   int restart = 0;
-  DBuf<double> V, Z, w, hdev, ydev;
-  DBuf<double> hpin_dummy;
-  double* hhost = nullptr;   // pinned
+  DBuf<double> V, Z, w, vin, zout;     // V [(r+1)][n], Z [r][n]; vin/zout: fixed pre in/out
+  DBuf<GmresScal> sc;
   void ensure(Dev& d, long long n_, int restart_);
-  ~Fgmres();
-  // x = 0 initial guess; stops when the Arnoldi residual <= tol*scale.
-  KrylovResult solve(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
-                     double scale, double tol, int maxit);
+  // Emit: x = FGMRES(op, pre) solution of op x = b from x0 = 0, stopping when the
+  // Arnoldi residual <= tol * (*scale) (scale: device scalar).  op / pre are
+  // capture functions (op(in, out), pre(in, out)); pre is always called with
+  // (vin, zout).  Nothing is read back.
+  void emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
+            const double* scale, double tol, int maxit);
+  void reset_total(Dev& d);
 };
 
-struct PcgSlices {
+// per-slice PCG device scalars: [slice] arrays + loop state
+struct PcgScal {
+  int it, maxit, flag;
+  int A_max;                  // max per-slice iteration count over the applies of one solve
+  long long A_total;          // sum of per-slice iteration counts over the applies of one solve
+};
+
+struct DevPcg {
   long long n = 0;
   int nslices = 0;
   DBuf<double> r, z, p, q;
-  DBuf<double> sc;        // per-slice scalars: bn rn rz rzn pq alpha beta active
-  DBuf<int> its, any;
-  // returns per-slice iteration counts (host)
-  std::vector<int> solve(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
-                         int nslices, long long slice_len, double tol, int maxit);
+  DBuf<double> s;             // [8][nslices]: bn rn rz pq alpha beta active tmp
+  DBuf<int> its;              // [nslices]
+  DBuf<PcgScal> sc;
+  void ensure(Dev& d, long long n_, int nslices_);
+  // Emit: per-slice PCG on the block-diagonal operator whose rows the view V
+  // yields (V::row), preconditioned by pre(r, z); x0 = 0; stop a slice at
+  // ||r^k|| <= tol ||b^k||; cap maxit.  Defined below.
+  template <class V>
+  void emit(Dev& d, Reducer& red, const V& view, const DevOp& pre, const double* b, double* x,
+            long long slice_len, double tol, int maxit);
+  void reset_stats(Dev& d);
 };
 
-// BLAS-1 helpers (deterministic)
+// BLAS-1 helpers
 void dev_copy(Dev& d, const double* a, double* b, long long n);
 void dev_scale(Dev& d, const double* a, double s, double* b, long long n);
 void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, long long n);  // b = alpha a + beta b
-double dev_norm(Dev& d, Reducer& red, const double* a, long long n, double* dscratch);
+// b = -a and *norm = ||a||_2 (one fused launch)
+void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n, double* norm);
+
+// ---- PCG kernel pieces shared with the operator emitter (solver.cu)
+// Layout of DevPcg::s (doubles, each [nslices]).
+enum { PS_BN = 0, PS_RN, PS_RZ, PS_PQ, PS_ALPHA, PS_BETA, PS_ACTIVE, PS_TMP, PS_COUNT };
+
+// Epilogue of the fused "p = z + beta p, q = A z + beta q, partial p.q" kernel:
+// alpha = rz / pq on active slices (a slice with pq <= 0 stops), its += active.
+struct PcgAlphaFin {
+  double* s;
+  int* its;
+  int ns;
+  __device__ void operator()(const double* out) const {
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+      double act = s[PS_ACTIVE * ns + k];
+      double pq = out[k];
+      if (act != 0.0 && !(pq > 0.0)) act = 0.0;
+      s[PS_ACTIVE * ns + k] = act;
+      s[PS_ALPHA * ns + k] = act != 0.0 ? s[PS_RZ * ns + k] / pq : 0.0;
+      its[k] += act != 0.0 ? 1 : 0;
+    }
+  }
+};
+
+// r = b, bn = ||b^k||, active = bn > 0, its = 0, it = 0; loop flag = any active
+__global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,
+                            PcgScal* P, int maxit, RedArgs R);
+// rz_new = r.z; beta (it > 0) and rz update
+__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, double* s,
+                         const PcgScal* P, RedArgs R);
+// x += alpha p, r -= alpha q; rn; active &= rn > tol bn; it++; loop condition; stats at exit
+__global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ q, double* s, const int* its, PcgScal* P, double tol, RedArgs R,
+                         LoopCtl L_);
+
+// p = z + beta p;  q = A z + beta q  (= A p, since q held A p_old);  partial p.q
+template <class V>
+__global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double* __restrict__ p,
+                         double* __restrict__ q, const double* __restrict__ s, RedArgs R, PcgAlphaFin fin) {
+  int k = blockIdx.y;
+  int ns = gridDim.y;
+  double beta = s[PS_BETA * ns + k];
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  double acc = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    long long row = (long long)k * L + i;
+    double az = 0.0;
+    v.row(row, [&](long long c, double a) { az += a * z[c]; });
+    double pv = z[row] + beta * p[row];
+    double qv = az + beta * q[row];
+    p[row] = pv;
+    q[row] = qv;
+    acc += pv * qv;
+  }
+  if (red_commit(acc, R)) fin(R.out);
+}
+
+template <class V>
+void DevPcg::emit(Dev& d, Reducer& red, const V& view, const DevOp& pre, const double* b, double* x,
+                  long long L, double tol, int maxit) {
+  const int ns = nslices;
+  const int BS = Reducer::BS;
+  int parts = red.parts_for(L, ns);
+  double* S = s.p;
+  double* out = S + PS_TMP * ns;
+  BB_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), d.stream));
+  BB_CUDA(cudaMemsetAsync(p.p, 0, n * sizeof(double), d.stream));
+  BB_CUDA(cudaMemsetAsync(q.p, 0, n * sizeof(double), d.stream));
+  launch(d, k_pcg_start, dim3(parts, ns), dim3(BS), 0, L, b, r.p, S, its.p, sc.p, maxit,
+         red.args(parts, ns, out));
+  dev_while(d, dev_field(sc.p, &PcgScal::flag), [&](const LoopCtl& ctl) {
+    pre(r.p, z.p);
+    launch(d, k_pcg_rz, dim3(parts, ns), dim3(BS), 0, L, (const double*)r.p, (const double*)z.p, S,
+           (const PcgScal*)sc.p, red.args(parts, ns, out));
+    launch(d, k_pcg_pq<V>, dim3(parts, ns), dim3(BS), 0, view, L, (const double*)z.p, p.p, q.p, (const double*)S,
+           red.args(parts, ns, out), PcgAlphaFin{S, its.p, ns});
+    launch(d, k_pcg_xr, dim3(parts, ns), dim3(BS), 0, L, x, r.p, (const double*)p.p, (const double*)q.p, S,
+           (const int*)its.p, sc.p, tol, red.args(parts, ns, out), ctl);
+  });
+}
 
 }  // namespace bbot

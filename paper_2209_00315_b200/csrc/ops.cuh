@@ -27,7 +27,8 @@ void check_state(bbot_ctx* c);
 
 // solver.cu
 void assemble_all(bbot_ctx* c, bbot_solve_stats* st);
-void bb_apply(bbot_ctx* c, const double* r, double* z);
-void solve(bbot_ctx* c, bbot_solve_stats* st);
+void bb_apply(bbot_ctx* c, const double* r, double* z, int* its_T, int* its_A_max);   // eager
+void solve(bbot_ctx* c, bbot_solve_stats* st);                                          // graph (or eager)
+void drop_solve_graph(bbot_ctx* c);
 
 }  // namespace bbot

@@ -1,6 +1,12 @@
 // solver.cu -- orchestration of one Newton system: assembly + BB setup (a1, a3),
 // the BB preconditioner apply (a4), FGMRES on (4.17) (a5), recovery (a6).
+//
+// The solve is *emitted* once per assembly into a CUDA graph (device loops as
+// conditional WHILE nodes, krylov.cuh) and replayed with one cudaGraphLaunch;
+// with the per-launch profiler on (or use_graph = false) the same emission runs
+// eagerly with the host reading the loop flags.
 #include "ops.cuh"
+#include <chrono>
 
 namespace bbot {
 
@@ -29,8 +35,16 @@ struct EvTimer {
 };
 }  // namespace
 
+void drop_solve_graph(bbot_ctx* c) {
+  if (c->solve_exec) {
+    cudaGraphExecDestroy(c->solve_exec);
+    c->solve_exec = nullptr;
+  }
+}
+
 void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   const bbot_solver_opts& o = c->opts;
+  drop_solve_graph(c);
   EvTimer t0(c->dev.stream);
   compute_residual(c, true);
   assemble_T(c);
@@ -41,6 +55,8 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
   double ts = t1.ms();
   c->as.valid = true;
+  c->t_assemble_ms = ta;
+  c->t_setup_ms = ts;
   if (st) {
     st->t_assemble_ms = ta;
     st->t_setup_ms = ts;
@@ -50,68 +66,139 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   }
 }
 
-void bb_apply(bbot_ctx* c, const double* r, double* z) {
+// workspaces of the solve (allocated outside any capture)
+static void prepare(bbot_ctx* c) {
+  const bbot_solver_opts& o = c->opts;
+  long long n = c->n(), m = c->m();
+  c->outer.ensure(c->dev, n + m, o.restart);
+  c->innerT.ensure(c->dev, m, o.restart_T);
+  c->pcg.ensure(c->dev, n, c->g.K + 1);
+  if (!c->nrm_T.p) c->nrm_T.alloc(4, c->dev.stream);
+}
+
+// a4: z = BB(r), r = (r1; r2), z = (x; y)  ((4.18)-(4.20), (4.26), A9, A12, A14)
+static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   const bbot_solver_opts& o = c->opts;
   long long n = c->n(), m = c->m();
   const double* r1 = r;
   const double* r2 = r + n;
   double* z1 = z;
   double* z2 = z + n;
-  // (i) T z = -r2, GMRES(restart_T) right-preconditioned by one AMG(T) V-cycle (4.26, A9)
-  dev_scale(c->dev, r2, -1.0, c->tmp_m.p, m);
-  double nr2 = dev_norm(c->dev, c->red, r2, m, c->scal.p);
+  // (i) T z2 = -r2, GMRES(restart_T) right-preconditioned by one AMG(T) V-cycle, relative eps_T
+  dev_neg_norm(c->dev, c->red, r2, c->tmp_m.p, m, c->nrm_T.p);
   SliceEllView vT = view_T(c);
-  c->innerT.ensure(c->dev, m, o.restart_T);
-  KrylovResult kt = c->innerT.solve(
+  c->innerT.emit(
       c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
-      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgT, vT, x, y); }, c->tmp_m.p, c->tmp_m2.p, nr2,
-      o.eps_T, o.maxit_inner);
-  c->bb_T_its += kt.its;
+      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgT, vT, x, y); }, c->tmp_m.p, c->tmp_m2.p,
+      c->nrm_T.p, o.eps_T, o.maxit_inner);
   // (ii) y = P^T Mbar^-1 Atilde z   (A12)
   bb_y_from_z(c, c->tmp_m2.p, z2);
   // (iii) b = r1 - B^T P^T y, slice means removed (compatibility)
   bb_rhs_A(c, r1, z2, c->tmp_n2.p);
-  // (iv) A_k x^k = b^k, per-slice PCG + AMG(A) V-cycle (4.20), then slice means removed
+  // (iv) A_k x^k = b^k: per-slice PCG + AMG(A) V-cycle (4.20), then slice means removed
   EdgeLapView vA = view_A(c);
-  std::vector<int> its = c->pcg.solve(
-      c->dev, c->red, [&](const double* x, double* y) { apply_A(c, x, y); },
-      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgA, vA, x, y); }, c->tmp_n2.p, z1, c->g.K + 1,
-      c->g.N, o.eps_A, o.maxit_inner);
-  for (int v : its) {
-    c->bb_A_max = std::max(c->bb_A_max, v);
-    c->bb_A_total += v;
-  }
+  c->pcg.emit(
+      c->dev, c->red, vA, [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgA, vA, x, y); },
+      c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner);
   remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
 }
 
-void solve(bbot_ctx* c, bbot_solve_stats* st) {
+// a5 + a6
+static void emit_solve(bbot_ctx* c) {
   const bbot_solver_opts& o = c->opts;
-  BB_REQUIRE(c->as.valid, BBOT_E_ORDER, "bbot_solve before bbot_assemble");
-  long long n = c->n(), m = c->m();
-  c->bb_T_its = 0;
-  c->bb_A_max = 0;
-  c->bb_A_total = 0;
-  c->outer.ensure(c->dev, n + m, o.restart);
-  EvTimer t0(c->dev.stream);
-  KrylovResult kr = c->outer.solve(
+  c->innerT.reset_total(c->dev);
+  c->pcg.reset_stats(c->dev);
+  c->outer.emit(
       c->dev, c->red, [&](const double* x, double* y) { jp_matvec(c, x, y); },
-      [&](const double* x, double* y) { bb_apply(c, x, y); }, c->as.rhs.p, c->sol.p, c->as.scale, o.eps_out,
-      o.maxit);
-  double tk = t0.ms();
-  EvTimer t1(c->dev.stream);
+      [&](const double* x, double* y) { emit_bb_apply(c, x, y); }, c->as.rhs.p, c->sol.p, c->as.dscale.p,
+      o.eps_out, o.maxit);
   recover(c);
-  double tr = t1.ms();
+}
+
+// Run `emit` either eagerly or as (captured once, then replayed) CUDA graph.
+template <class Emit>
+static void run_emitted(bbot_ctx* c, cudaGraphExec_t* cache, Emit&& emit) {
+  Dev& d = c->dev;
+  bool graph = c->use_graph && !d.prof && cache != nullptr;
+  c->t_capture_ms = 0;
+  if (!graph) {
+    emit();
+    return;
+  }
+  if (!*cache) {
+    auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t user = d.stream;
+    cudaStream_t cap = capture_stream(d, 0);
+    BB_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+    d.stream = cap;
+    d.capturing = true;
+    d.depth = 0;
+    cudaGraph_t g = nullptr;
+    try {
+      emit();
+    } catch (...) {
+      d.stream = user;
+      d.capturing = false;
+      cudaStreamEndCapture(cap, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    d.stream = user;
+    d.capturing = false;
+    BB_CUDA(cudaStreamEndCapture(cap, &g));
+    cudaError_t e = cudaGraphInstantiate(cache, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      *cache = nullptr;
+      throw Error(BBOT_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    c->t_capture_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  BB_CUDA(cudaGraphLaunch(*cache, d.stream));
+}
+
+void bb_apply(bbot_ctx* c, const double* r, double* z, int* its_T, int* its_A_max) {
+  prepare(c);
+  c->innerT.reset_total(c->dev);
+  c->pcg.reset_stats(c->dev);
+  emit_bb_apply(c, r, z);
+  GmresScal gT;
+  PcgScal pA;
+  BB_CUDA(cudaMemcpyAsync(&gT, c->innerT.sc.p, sizeof(gT), cudaMemcpyDeviceToHost, c->dev.stream));
+  BB_CUDA(cudaMemcpyAsync(&pA, c->pcg.sc.p, sizeof(pA), cudaMemcpyDeviceToHost, c->dev.stream));
+  sync(c->dev);
+  if (its_T) *its_T = (int)gT.total_its;
+  if (its_A_max) *its_A_max = pA.A_max;
+}
+
+void solve(bbot_ctx* c, bbot_solve_stats* st) {
+  BB_REQUIRE(c->as.valid, BBOT_E_ORDER, "bbot_solve before bbot_assemble");
+  prepare(c);
+  EvTimer t0(c->dev.stream);
+  run_emitted(c, &c->solve_exec, [&]() { emit_solve(c); });
+  double tk = t0.ms();
+  GmresScal gO, gT;
+  PcgScal pA;
+  BB_CUDA(cudaMemcpyAsync(&gO, c->outer.sc.p, sizeof(gO), cudaMemcpyDeviceToHost, c->dev.stream));
+  BB_CUDA(cudaMemcpyAsync(&gT, c->innerT.sc.p, sizeof(gT), cudaMemcpyDeviceToHost, c->dev.stream));
+  BB_CUDA(cudaMemcpyAsync(&pA, c->pcg.sc.p, sizeof(pA), cudaMemcpyDeviceToHost, c->dev.stream));
+  sync(c->dev);
   c->have_dir = true;
   if (st) {
-    st->outer_its = kr.its;
-    st->inner_T_its = c->bb_T_its;
-    st->inner_A_its_max = c->bb_A_max;
-    st->inner_A_its_total = c->bb_A_total;
-    st->converged = kr.converged ? 1 : 0;
+    st->outer_its = gO.its;
+    st->inner_T_its = (int)gT.total_its;
+    st->inner_A_its_max = pA.A_max;
+    st->inner_A_its_total = pA.A_total;
+    st->converged = gO.conv ? 1 : 0;
     st->scale = c->as.scale;
-    st->rel_res = c->as.scale > 0 ? kr.res / c->as.scale : 0.0;
+    st->rel_res = c->as.scale > 0 ? gO.res / c->as.scale : 0.0;
     st->t_krylov_ms = tk;
-    st->t_recover_ms = tr;
+    st->t_recover_ms = 0.0;   // recovery is part of the emitted solve
+    st->t_assemble_ms = c->t_assemble_ms;
+    st->t_setup_ms = c->t_setup_ms;
+    st->amg_levels_A = (int)c->amgA.lv.size();
+    st->amg_levels_T = (int)c->amgT.lv.size();
+    st->t_graph_ms = c->t_capture_ms;
   }
 }
 

@@ -147,6 +147,31 @@ def test_newton_direction_parity(name, mu):
         assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+def test_graph_and_eager_solves_identical():
+    """The captured CUDA-graph solve (device-side loops) and the eager issue of
+    the same kernels give bitwise-identical directions and identical counts."""
+    pb = _gpu()
+    p, d, phi, rho, s = ipm_state("C1", 2.0 ** -3)
+    out = []
+    for graph in (True, False):
+        ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+        ctx.set_exec_mode(graph)
+        ctx.set_state(phi, rho, s, 2.0 ** -4)
+        ctx.assemble()
+        out.append(ctx.solve())
+        if graph:   # replay of the same graph on a re-assembled identical system
+            ctx.set_state(phi, rho, s, 2.0 ** -4)
+            ctx.assemble()
+            again = ctx.solve()
+            for a, b in zip(again[:3], out[0][:3]):
+                assert np.array_equal(a, b)
+    (g1, g2, g3, gs), (e1, e2, e3, es) = out
+    for a, b in ((g1, e1), (g2, e2), (g3, e3)):
+        assert np.array_equal(a, b)
+    for k in ("outer_its", "inner_T_its", "inner_A_its_max", "inner_A_its_total", "converged"):
+        assert gs[k] == es[k], k
+
+
 def test_newton_update_and_ke_parity():
     """a7 step (alpha, update, renormalisation) and D12."""
     from oracle.ipm import renormalise, step_length
@@ -198,3 +223,43 @@ def test_state_errors():
     ctx2 = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     with pytest.raises(pb.BbotError):
         ctx2.solve()          # before assemble -> BBOT_E_ORDER
+
+
+def test_ipm_parity_C1_full():
+    """Full IPM on BASELINE configs[0] (C1: 512 cells, K = 8, mu 1 -> 2^-26 ~ 1.49e-8,
+    A17-A20): number of Newton systems equal, every system's outer count +-1 while
+    both sides converge, final kinetic energy to 1e-6 (north star)."""
+    from oracle.ipm import IpmOpts, ipm_run
+    pb = _gpu()
+    p = make_problem("C1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    res = ipm_run(d, phi, rho, s, IpmOpts(), SolverOpts())
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts())
+    assert st["n_systems"] == len(res.log)
+    for g, o in zip(log, res.log):
+        if o["converged"] and g["converged"]:
+            assert abs(g["outer_its"] - o["outer_its"]) <= 1, (g, o)
+    assert abs(st["kinetic_energy"] - res.kinetic_energy) <= 1e-6 * abs(res.kinetic_energy)
+
+
+def test_direction_parity_C2_bench_system():
+    """The bench workload itself (BASELINE configs[1], C2: 8192 cells, K = 32,
+    1.07 M unknowns, jittered mesh): the first IPM Newton system at the A19 point,
+    solved in the bench's launch configuration (CUDA graph), against the oracle."""
+    pb = _gpu()
+    p = make_problem("C2")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    ctx.assemble()
+    dphi, drho, ds, st = ctx.solve()
+    S = BBSolver(d, phi, rho, s, 1.0, SolverOpts())
+    ophi, orho, os_ = S.solve()
+    assert S.stats["converged"] and st["converged"] == 1
+    assert abs(st["outer_its"] - S.stats["outer_its"]) <= 1, (st, S.stats)
+    for a, b in ((dphi, ophi), (drho, orho), (ds, os_)):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
