@@ -4,6 +4,8 @@
 // independently.
 #include "amg.cuh"
 #include <climits>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace bbot {
 
@@ -251,6 +253,27 @@ __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restr
   xo[r] = (x[r] + xc[agg[r]]) + om * dinv[r] * acc;
 }
 
+// level-0 prolongation + post-smoothing fused with the per-slice dot b.xo
+// (grid (parts, ns) over slice-major rows; PCG: r.z with its beta epilogue)
+template <class V>
+__global__ void k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                         const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
+                         double* __restrict__ xo, long long L, RedArgs R, PcgRzFin fin) {
+  int k = blockIdx.y;
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  double dot = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    long long r = (long long)k * L + i;
+    double acc = b[r];
+    v.row(r, [&](long long c, double a) { acc -= a * (x[c] + xc[agg[c]]); });
+    double z = (x[r] + xc[agg[r]]) + om * dinv[r] * acc;
+    xo[r] = z;
+    dot += b[r] * z;
+  }
+  if (red_commit(dot, R)) fin(R.out);
+}
+
 // ------------------------------------------------------------ coarsest
 // mode A: per slice, grounded at the slice's first row; Gauss-Jordan with partial
 // pivoting on [B | I] in shared memory, B = block without row/col 0.
@@ -334,6 +357,120 @@ __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, cons
   for (int j = threadIdx.x; j < nloc; j += blockDim.x) x[s0 + j] = xs[j] - mean;
 }
 
+// ------------------------------------------------------------ per-slice coarse tail (mode A)
+// AMG(A) never aggregates across time slices (I3), so below the level where a
+// slice has <= TAIL_ROWS rows the rest of the V-cycle is independent per slice:
+// one CTA per slice runs restriction from level tail-1, every coarser level's
+// pre-smoothing + residual + restriction, the grounded coarsest solve, and the
+// prolongation + post-smoothing back up to level `tail`, separated by
+// __syncthreads() instead of kernel launches.  Arithmetic is the same per row as
+// k_down / k_restrict / k_coarseA_apply / k_up (same operation order).
+constexpr int TAIL_ROWS = 8192;
+constexpr int TAIL_MAXL = 24;
+constexpr int TAIL_BS = 1024;
+
+struct TailLevel {
+  const long long* rp;
+  const int* ci;
+  const double* v;
+  const double* dinv;
+  double *b, *x, *r, *xo;      // xo: level output (xt, or x at the coarsest)
+  const long long* mptr;       // coarse row -> members (restriction to the next level)
+  const int* midx;
+  const int* agg;
+  const long long* sptr;       // device slice pointers
+};
+struct TailArgs {
+  int first, last;             // levels first..last (last = coarsest)
+  double om;
+  int cm;
+  const double* cinv;
+  // restriction into level `first` from level first-1
+  const long long* mptr0;
+  const int* midx0;
+  const double* r0;
+  TailLevel lv[TAIL_MAXL];
+};
+
+__global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
+  const int k = blockIdx.x;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  const double om = T.om;
+  // restriction from level first-1 (rows of slice k at level `first` are contiguous)
+  {
+    const TailLevel& F = T.lv[0];
+    long long s0 = F.sptr[k], s1 = F.sptr[k + 1];
+    for (long long I = s0 + tid; I < s1; I += bs) {
+      double acc = 0.0;
+      for (long long p = T.mptr0[I]; p < T.mptr0[I + 1]; p++) acc += T.r0[T.midx0[p]];
+      F.b[I] = acc;
+    }
+  }
+  __syncthreads();
+  const int nl = T.last - T.first;     // levels with smoothing (coarsest excluded)
+  for (int q = 0; q < nl; q++) {
+    const TailLevel& L = T.lv[q];
+    long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
+    for (long long r = s0 + tid; r < s1; r += bs) {
+      double acc = L.b[r];
+      for (long long p = L.rp[r]; p < L.rp[r + 1]; p++) {
+        int c = L.ci[p];
+        acc -= L.v[p] * (om * L.dinv[c] * L.b[c]);
+      }
+      L.x[r] = om * L.dinv[r] * L.b[r];
+      L.r[r] = acc;
+    }
+    __syncthreads();
+    const TailLevel& C = T.lv[q + 1];
+    long long c0 = C.sptr[k], c1 = C.sptr[k + 1];
+    for (long long I = c0 + tid; I < c1; I += bs) {
+      double acc = 0.0;
+      for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
+      C.b[I] = acc;
+    }
+    __syncthreads();
+  }
+  // coarsest: grounded at the slice's first row, then the slice mean removed
+  {
+    __shared__ double xs[128];
+    __shared__ double mean;
+    const TailLevel& C = T.lv[nl];
+    long long s0 = C.sptr[k];
+    int nloc = (int)(C.sptr[k + 1] - s0);
+    const double* inv = T.cinv + (size_t)k * T.cm * T.cm;
+    for (int j = tid; j < nloc; j += bs) {
+      double acc = 0.0;
+      if (j > 0)
+        for (int l = 1; l < nloc; l++) acc += inv[(j - 1) * T.cm + (l - 1)] * C.b[s0 + l];
+      xs[j] = acc;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double sum = 0.0;
+      for (int j = tid; j < nloc; j += 32) sum += xs[j];
+      sum = warp_sum(sum);
+      if (tid == 0) mean = nloc > 0 ? sum / nloc : 0.0;
+    }
+    __syncthreads();
+    for (int j = tid; j < nloc; j += bs) C.xo[s0 + j] = xs[j] - mean;
+    __syncthreads();
+  }
+  for (int q = nl - 1; q >= 0; q--) {
+    const TailLevel& L = T.lv[q];
+    const double* xc = T.lv[q + 1].xo;
+    long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
+    for (long long r = s0 + tid; r < s1; r += bs) {
+      double acc = L.b[r];
+      for (long long p = L.rp[r]; p < L.rp[r + 1]; p++) {
+        int c = L.ci[p];
+        acc -= L.v[p] * (L.x[c] + xc[L.agg[c]]);
+      }
+      L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
+    }
+    __syncthreads();
+  }
+}
+
 // mode T: dense Gauss-Jordan in global memory, two launches per pivot
 __global__ void k_csr_to_dense(CsrView A, int n, double* D, double* I) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -342,56 +479,86 @@ __global__ void k_csr_to_dense(CsrView A, int n, double* D, double* I) {
   I[r * n + r] = 1.0;
 }
 
-__global__ void k_gj_pivot(int n, int p, double* D, double* I, double* fcol) {
-  __shared__ double bv[1024];
-  __shared__ int bi[1024];
-  double best = -1.0;
-  int besti = p;
-  for (int i = p + threadIdx.x; i < n; i += blockDim.x) {
-    double v = fabs(D[(size_t)i * n + p]);
-    if (v > best) { best = v; besti = i; }
-  }
-  bv[threadIdx.x] = best;
-  bi[threadIdx.x] = besti;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      double v2 = bv[threadIdx.x + o];
-      int i2 = bi[threadIdx.x + o];
-      if (v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < bi[threadIdx.x])) {
-        bv[threadIdx.x] = v2;
-        bi[threadIdx.x] = i2;
+// Gauss-Jordan inverse with partial pivoting as ONE cooperative launch (one grid
+// barrier per pivot instead of two launches).  Rows are not swapped: the pivot
+// of column p is the unused row of largest |D[i][p]| (ties -> lower index); every
+// other row is eliminated against it; each block, having updated its own rows,
+// already proposes its candidate for column p+1, so a step needs one barrier.
+// At the end pivot row piv[p] holds D[piv[p]][p] e_p^T | (that multiple of row p
+// of the inverse): inv[p][:] = I[piv[p]][:] / D[piv[p]][p].
+constexpr int GJ_BS = 256;
+__global__ void __launch_bounds__(GJ_BS) k_gj_coop(int n, double* D, double* I, double* cand_v, int* cand_i,
+                                                    int* used, int* piv, double* out) {
+  cg::grid_group grid = cg::this_grid();
+  const int nb = gridDim.x, tid = threadIdx.x;
+  __shared__ double sv[GJ_BS];
+  __shared__ int si[GJ_BS];
+  __shared__ int s_piv;
+  // rows owned by this block: i = blockIdx.x + q*nb
+  auto propose = [&](int col) {
+    double best = -1.0;
+    int bi = INT_MAX;
+    for (int i = blockIdx.x + tid * nb; i < n; i += nb * GJ_BS) {
+      if (used[i]) continue;
+      double v = fabs(D[(size_t)i * n + col]);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+    sv[tid] = best;
+    si[tid] = bi;
+    __syncthreads();
+    for (int o = GJ_BS / 2; o > 0; o >>= 1) {
+      if (tid < o) {
+        double v2 = sv[tid + o];
+        int i2 = si[tid + o];
+        if (v2 > sv[tid] || (v2 == sv[tid] && i2 < si[tid])) { sv[tid] = v2; si[tid] = i2; }
       }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      cand_v[(col & 1) * nb + blockIdx.x] = sv[0];
+      cand_i[(col & 1) * nb + blockIdx.x] = si[0];
     }
     __syncthreads();
-  }
-  int piv = bi[0];
-  if (piv != p)
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      double t = D[(size_t)p * n + j]; D[(size_t)p * n + j] = D[(size_t)piv * n + j]; D[(size_t)piv * n + j] = t;
-      t = I[(size_t)p * n + j]; I[(size_t)p * n + j] = I[(size_t)piv * n + j]; I[(size_t)piv * n + j] = t;
+  };
+  propose(0);
+  grid.sync();
+  for (int p = 0; p < n; p++) {
+    if (tid == 0) {   // every block reduces the candidates identically
+      double best = -1.0;
+      int bi = INT_MAX;
+      for (int b = 0; b < nb; b++) {
+        double v = cand_v[(p & 1) * nb + b];
+        int i = cand_i[(p & 1) * nb + b];
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      s_piv = bi;
     }
-  __syncthreads();
-  double pv = D[(size_t)p * n + p];
-  __syncthreads();
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    D[(size_t)p * n + j] /= pv;
-    I[(size_t)p * n + j] /= pv;
+    __syncthreads();
+    const int pr = s_piv;
+    const double pv = D[(size_t)pr * n + p];
+    // eliminate column p from every other row owned by this block
+    for (int i = blockIdx.x; i < n; i += nb) {
+      if (i == pr) continue;
+      double f = D[(size_t)i * n + p] / pv;
+      if (f == 0.0) continue;
+      for (int j = tid; j < n; j += GJ_BS) {
+        if (j > p) D[(size_t)i * n + j] -= f * D[(size_t)pr * n + j];
+        I[(size_t)i * n + j] -= f * I[(size_t)pr * n + j];
+      }
+      __syncthreads();
+      if (tid == 0) D[(size_t)i * n + p] = 0.0;
+    }
+    if (tid == 0 && blockIdx.x == 0) piv[p] = pr;
+    if (blockIdx.x == pr % nb && tid == 0) used[pr] = 1;
+    __syncthreads();
+    if (p + 1 < n) propose(p + 1);
+    grid.sync();
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) fcol[i] = (i == p) ? 0.0 : D[(size_t)i * n + p];
-}
-
-__global__ void k_gj_elim(int n, int p, double* D, double* I, const double* __restrict__ fcol) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long tot = (long long)n * n;
-  if (t >= tot) return;
-  int i = (int)(t / n), j = (int)(t - (long long)i * n);
-  if (i == p) return;
-  double f = fcol[i];
-  if (f == 0.0) return;
-  if (j > p) D[(size_t)i * n + j] -= f * D[(size_t)p * n + j];
-  else if (j == p) D[(size_t)i * n + j] = 0.0;
-  I[(size_t)i * n + j] -= f * I[(size_t)p * n + j];
+  for (long long t = (long long)blockIdx.x * GJ_BS + tid; t < (long long)n * n; t += (long long)nb * GJ_BS) {
+    int r = (int)(t / n), j = (int)(t - (long long)r * n);
+    int pr = piv[r];
+    out[t] = I[(size_t)pr * n + j] / D[(size_t)pr * n + r];
+  }
 }
 
 __global__ void k_dense_mv(int n, const double* __restrict__ A, const double* __restrict__ b, double* x) {
@@ -615,18 +782,55 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     long long n = C.n;
     BB_REQUIRE(n <= 8192, BBOT_E_INTERNAL, "AMG(T): coarsest level too large");
     H.cm = (int)n;
-    DBuf<double> D, fcol;
+    DBuf<double> D;
     D.alloc((size_t)n * n, s);
     D.zero();
     H.cinv.alloc((size_t)n * n, s);
-    H.cinv.zero();
-    fcol.alloc(n, s);
-    launch(d, k_csr_to_dense, dim3(nblocks(n, BS)), dim3(BS), 0, C.view(), (int)n, D.p, H.cinv.p);
-    for (int p = 0; p < n; p++) {
-      launch(d, k_gj_pivot, dim3(1), dim3(1024), 0, (int)n, p, D.p, H.cinv.p, fcol.p);
-      launch(d, k_gj_elim, dim3(nblocks(n * n, BS)), dim3(BS), 0, (int)n, p, D.p, H.cinv.p, (const double*)fcol.p);
-    }
+    DBuf<double> Iw, cv;
+    DBuf<int> ci, used, piv;
+    Iw.alloc((size_t)n * n, s);
+    Iw.zero();
+    launch(d, k_csr_to_dense, dim3(nblocks(n, BS)), dim3(BS), 0, C.view(), (int)n, D.p, Iw.p);
+    int per_sm = 0;
+    BB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, GJ_BS, 0));
+    int nbk = std::max(1, std::min(per_sm * d.num_sms, (int)std::min<long long>(n, 2 * d.num_sms)));
+    cv.alloc(2 * (size_t)nbk, s);
+    ci.alloc(2 * (size_t)nbk, s);
+    used.alloc(n, s);
+    used.zero();
+    piv.alloc(n, s);
+    int ni = (int)n;
+    double* Dp = D.p;
+    double* Ip = Iw.p;
+    double* cvp = cv.p;
+    int* cip = ci.p;
+    int* up = used.p;
+    int* pp = piv.p;
+    double* op = H.cinv.p;
+    void* args[] = {&ni, &Dp, &Ip, &cvp, &cip, &up, &pp, &op};
+    BB_CUDA(cudaLaunchCooperativeKernel((const void*)k_gj_coop, dim3(nbk), dim3(GJ_BS), args, 0, d.stream));
+    d.launches++;
     sync(d);
+  }
+  // mode A: the per-slice tail starts at the first coarse level with <= TAIL_ROWS rows per slice
+  H.tail = 0;
+  if (mode == 0 && H.lv.size() >= 2) {
+    int L = (int)H.lv.size();
+    for (int l = 1; l < L; l++) {
+      long long mx = 0;
+      for (int k = 0; k < nslices; k++) mx = std::max(mx, H.lv[l].sptr[k + 1] - H.lv[l].sptr[k]);
+      if (mx <= TAIL_ROWS && L - l <= TAIL_MAXL) {
+        H.tail = l;
+        break;
+      }
+    }
+    for (int l = std::max(1, H.tail); H.tail > 0 && l < L; l++) {
+      AmgLevel& A = H.lv[l];
+      A.dsptr.alloc(nslices + 1, s);
+      BB_CUDA(cudaMemcpyAsync(A.dsptr.p, A.sptr.data(), (nslices + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                              s));
+    }
+    sync(d);   // the host slice-pointer vectors are sources of the async copies above
   }
   H.ready = true;
 }
@@ -641,12 +845,48 @@ static void coarse_solve(Dev& d, AmgHierarchy& H, const double* b, double* x) {
            (const double*)H.cinv.p, b, x);
 }
 
-template <class V0>
-void amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x) {
+// output buffer of level l in the V-cycle (no buffer swapping: capture-safe)
+static double* level_out(AmgHierarchy& H, int l) {
+  return l == (int)H.lv.size() - 1 ? H.lv[l].x.p : H.lv[l].xt.p;
+}
+
+static void tail_args(AmgHierarchy& H, TailArgs& T) {
   int L = (int)H.lv.size();
-  if (L == 1) { coarse_solve(d, H, b, x); return; }
+  T.first = H.tail;
+  T.last = L - 1;
+  T.om = H.omega;
+  T.cm = H.cm;
+  T.cinv = H.cinv.p;
+  AmgLevel& P = H.lv[H.tail - 1];
+  T.mptr0 = P.mptr.p;
+  T.midx0 = P.midx.p;
+  T.r0 = P.r.p;
+  for (int l = H.tail; l < L; l++) {
+    AmgLevel& A = H.lv[l];
+    TailLevel& t = T.lv[l - H.tail];
+    t.rp = A.rp.p;
+    t.ci = A.ci.p;
+    t.v = A.v.p;
+    t.dinv = A.dinv.p;
+    t.b = A.b.p;
+    t.x = A.x.p;
+    t.r = A.r.p;
+    t.xo = level_out(H, l);
+    t.mptr = A.mptr.p;
+    t.midx = A.midx.p;
+    t.agg = A.agg.p;
+    t.sptr = A.dsptr.p;
+  }
+}
+
+template <class V0>
+bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, const SliceDotFuse* fuse) {
+  int L = (int)H.lv.size();
+  if (L == 1) { coarse_solve(d, H, b, x); return false; }
   double om = H.omega;
-  for (int l = 0; l < L - 1; l++) {
+  // grid-wide levels: 0 .. stop-1; below: the per-slice tail (mode A) or more grid levels
+  int stop = (H.mode == 0 && H.tail > 0) ? H.tail : L - 1;
+  for (int l = 0; l < stop; l++) {
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
     if (l == 0)
@@ -654,30 +894,43 @@ void amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     else
       launch(d, k_down<CsrView>, dim3(nb), dim3(BS), 0, lv.view(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, lv.x.p, lv.r.p);
-    launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
-           (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p);
+    if (!(H.mode == 0 && H.tail > 0 && l == stop - 1))
+      launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
+             (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p);
   }
-  coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
-  for (int l = L - 2; l >= 0; l--) {
+  if (H.mode == 0 && H.tail > 0) {
+    TailArgs T;
+    tail_args(H, T);
+    launch(d, k_tailA, dim3(H.nslices), dim3(TAIL_BS), 0, T);
+  } else {
+    coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
+  }
+  for (int l = stop - 1; l >= 0; l--) {
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
-    if (l == 0) {
+    double* out = l == 0 ? x : level_out(H, l);
+    const double* xc = level_out(H, l + 1);
+    if (l == 0 && fuse) {
+      launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
+             (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin);
+    } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
-             (const int*)lv.agg.p, (const double*)H.lv[1].x.p, x);
+             (const int*)lv.agg.p, xc, out);
     } else {
       launch(d, k_up<CsrView>, dim3(nb), dim3(BS), 0, lv.view(), (const double*)lv.dinv.p,
-             (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p,
-             (const double*)H.lv[l + 1].x.p, lv.xt.p);
-      std::swap(lv.x, lv.xt);
+             (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p, xc, out);
     }
   }
+  return fuse != nullptr;
 }
 
 template void amg_setup<EdgeLapView>(Dev&, AmgHierarchy&, const EdgeLapView&, const int*, int, int, double, int,
                                      AmgWork&);
 template void amg_setup<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const int*, int, int, double, int,
                                       AmgWork&);
-template void amg_vcycle<EdgeLapView>(Dev&, AmgHierarchy&, const EdgeLapView&, const double*, double*);
-template void amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*);
+template bool amg_vcycle<EdgeLapView>(Dev&, AmgHierarchy&, const EdgeLapView&, const double*, double*,
+                                      const SliceDotFuse*);
+template bool amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*,
+                                       const SliceDotFuse*);
 
 }  // namespace bbot

@@ -13,6 +13,7 @@
 // (SliceEllView).  Coarse levels are CSR (int64 row pointers).
 #pragma once
 #include "common.cuh"
+#include "pcg_fin.cuh"
 
 namespace bbot {
 
@@ -89,8 +90,9 @@ struct AmgLevel {
   DBuf<int> agg;          // row -> coarse row (not at the coarsest)
   DBuf<long long> mptr;   // coarse row -> members (ascending)
   DBuf<int> midx;
-  DBuf<double> b, x, r, xt;
+  DBuf<double> b, x, r, xt;      // x: pre-smoothed iterate; xt: this level's V-cycle output
   std::vector<long long> sptr;   // host slice pointers
+  DBuf<long long> dsptr;         // the same on the device (per-slice coarse tail)
   CsrView view() const { return CsrView{n, rp.p, ci.p, v.p}; }
 };
 
@@ -103,6 +105,7 @@ struct AmgHierarchy {
   DBuf<double> cinv;       // mode A: [nslices][cm][cm] (grounded), mode T: [nc][nc]
   int cm = 0;              // mode A: max rows per slice - 1; mode T: nc
   DBuf<long long> csptr;   // mode A: coarsest slice pointers (device)
+  int tail = 0;            // mode A: first level handled by the per-slice tail kernel
   bool ready = false;
   void clear() { lv.clear(); ready = false; }
 };
@@ -116,7 +119,11 @@ struct AmgWork {
 template <class V0>
 void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nslices, int mode,
                double omega, int coarse_max, AmgWork& w);
+// x = one V(1,1) cycle applied to b.  If fuse != nullptr (level-0 rows are
+// slice-major, fuse->L per slice) the last kernel also reduces b.x per slice and
+// runs fuse->fin (the PCG r.z step); returns true iff it did.
 template <class V0>
-void amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x);
+bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x,
+                const SliceDotFuse* fuse = nullptr);
 
 }  // namespace bbot

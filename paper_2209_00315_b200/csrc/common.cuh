@@ -287,7 +287,8 @@ struct Reducer {
   static constexpr int BS = 256;
   void init(Dev* d, int max_slices) {
     dev = d;
-    cap = (size_t)8 * d->num_sms + 2 * (size_t)max_slices + 4096;
+    // (parts <= 1024) x (<= 33 CGS2 dots) covers every multi-result reduction
+    cap = std::max((size_t)8 * d->num_sms + 2 * (size_t)max_slices + 4096, (size_t)1024 * 33);
     partial.alloc(cap, d->stream);
     counter.alloc(1, d->stream);
     counter.zero();

@@ -303,28 +303,14 @@ __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* _
   }
 }
 
-__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, double* s,
-                         const PcgScal* P, RedArgs R) {
+__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, RedArgs R,
+                         PcgRzFin fin) {
   int k = blockIdx.y;
-  const int ns = gridDim.y;
   long long beg, end;
   red_chunk(L, R.parts, beg, end);
   double acc = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) acc += r[(size_t)k * L + i] * z[(size_t)k * L + i];
-  if (!red_commit(acc, R)) return;
-  const int it = P->it;
-  for (int q = threadIdx.x; q < ns; q += blockDim.x) {
-    double rzn = R.out[q];
-    if (it == 0) {
-      s[PS_RZ * ns + q] = rzn;
-      s[PS_BETA * ns + q] = 0.0;
-    } else {
-      double act = s[PS_ACTIVE * ns + q];
-      double rz = s[PS_RZ * ns + q];
-      s[PS_BETA * ns + q] = act != 0.0 ? rzn / (rz != 0.0 ? rz : 1.0) : 0.0;
-      if (act != 0.0) s[PS_RZ * ns + q] = rzn;
-    }
-  }
+  if (red_commit(acc, R)) fin(R.out);
 }
 
 __global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,

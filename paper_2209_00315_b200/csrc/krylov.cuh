@@ -13,6 +13,7 @@
 // same data and give bitwise-identical results.
 #pragma once
 #include "common.cuh"
+#include "pcg_fin.cuh"
 #include <functional>
 
 namespace bbot {
@@ -48,13 +49,6 @@ struct DevGmres {
   void reset_total(Dev& d);
 };
 
-// per-slice PCG device scalars: [slice] arrays + loop state
-struct PcgScal {
-  int it, maxit, flag;
-  int A_max;                  // max per-slice iteration count over the applies of one solve
-  long long A_total;          // sum of per-slice iteration counts over the applies of one solve
-};
-
 struct DevPcg {
   long long n = 0;
   int nslices = 0;
@@ -66,8 +60,11 @@ struct DevPcg {
   // Emit: per-slice PCG on the block-diagonal operator whose rows the view V
   // yields (V::row), preconditioned by pre(r, z); x0 = 0; stop a slice at
   // ||r^k|| <= tol ||b^k||; cap maxit.  Defined below.
-  template <class V>
-  void emit(Dev& d, Reducer& red, const V& view, const DevOp& pre, const double* b, double* x,
+  // pre(r, z, fuse): z = M r; if fuse != nullptr the preconditioner must also
+  // emit the per-slice reduction r.z with fuse's epilogue (fused into its last
+  // kernel), else the PCG launches it separately.
+  template <class V, class Pre>
+  void emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const double* b, double* x,
             long long slice_len, double tol, int maxit);
   void reset_stats(Dev& d);
 };
@@ -79,34 +76,12 @@ void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, lo
 // b = -a and *norm = ||a||_2 (one fused launch)
 void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n, double* norm);
 
-// ---- PCG kernel pieces shared with the operator emitter (solver.cu)
-// Layout of DevPcg::s (doubles, each [nslices]).
-enum { PS_BN = 0, PS_RN, PS_RZ, PS_PQ, PS_ALPHA, PS_BETA, PS_ACTIVE, PS_TMP, PS_COUNT };
-
-// Epilogue of the fused "p = z + beta p, q = A z + beta q, partial p.q" kernel:
-// alpha = rz / pq on active slices (a slice with pq <= 0 stops), its += active.
-struct PcgAlphaFin {
-  double* s;
-  int* its;
-  int ns;
-  __device__ void operator()(const double* out) const {
-    for (int k = threadIdx.x; k < ns; k += blockDim.x) {
-      double act = s[PS_ACTIVE * ns + k];
-      double pq = out[k];
-      if (act != 0.0 && !(pq > 0.0)) act = 0.0;
-      s[PS_ACTIVE * ns + k] = act;
-      s[PS_ALPHA * ns + k] = act != 0.0 ? s[PS_RZ * ns + k] / pq : 0.0;
-      its[k] += act != 0.0 ? 1 : 0;
-    }
-  }
-};
-
 // r = b, bn = ||b^k||, active = bn > 0, its = 0, it = 0; loop flag = any active
 __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,
                             PcgScal* P, int maxit, RedArgs R);
 // rz_new = r.z; beta (it > 0) and rz update
-__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, double* s,
-                         const PcgScal* P, RedArgs R);
+__global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, RedArgs R,
+                         PcgRzFin fin);
 // x += alpha p, r -= alpha q; rn; active &= rn > tol bn; it++; loop condition; stats at exit
 __global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                          const double* __restrict__ q, double* s, const int* its, PcgScal* P, double tol, RedArgs R,
@@ -135,8 +110,8 @@ __global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double*
   if (red_commit(acc, R)) fin(R.out);
 }
 
-template <class V>
-void DevPcg::emit(Dev& d, Reducer& red, const V& view, const DevOp& pre, const double* b, double* x,
+template <class V, class Pre>
+void DevPcg::emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const double* b, double* x,
                   long long L, double tol, int maxit) {
   const int ns = nslices;
   const int BS = Reducer::BS;
@@ -149,9 +124,9 @@ void DevPcg::emit(Dev& d, Reducer& red, const V& view, const DevOp& pre, const d
   launch(d, k_pcg_start, dim3(parts, ns), dim3(BS), 0, L, b, r.p, S, its.p, sc.p, maxit,
          red.args(parts, ns, out));
   dev_while(d, dev_field(sc.p, &PcgScal::flag), [&](const LoopCtl& ctl) {
-    pre(r.p, z.p);
-    launch(d, k_pcg_rz, dim3(parts, ns), dim3(BS), 0, L, (const double*)r.p, (const double*)z.p, S,
-           (const PcgScal*)sc.p, red.args(parts, ns, out));
+    SliceDotFuse fz{red.args(parts, ns, out), parts, ns, L, PcgRzFin{S, sc.p, ns}};
+    if (!pre(r.p, z.p, &fz))
+      launch(d, k_pcg_rz, dim3(parts, ns), dim3(BS), 0, L, (const double*)r.p, (const double*)z.p, fz.R, fz.fin);
     launch(d, k_pcg_pq<V>, dim3(parts, ns), dim3(BS), 0, view, L, (const double*)z.p, p.p, q.p, (const double*)S,
            red.args(parts, ns, out), PcgAlphaFin{S, its.p, ns});
     launch(d, k_pcg_xr, dim3(parts, ns), dim3(BS), 0, L, x, r.p, (const double*)p.p, (const double*)q.p, S,

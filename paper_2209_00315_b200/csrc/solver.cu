@@ -98,7 +98,8 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   // (iv) A_k x^k = b^k: per-slice PCG + AMG(A) V-cycle (4.20), then slice means removed
   EdgeLapView vA = view_A(c);
   c->pcg.emit(
-      c->dev, c->red, vA, [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgA, vA, x, y); },
+      c->dev, c->red, vA,
+      [&](const double* x, double* y, const SliceDotFuse* f) { return amg_vcycle(c->dev, c->amgA, vA, x, y, f); },
       c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner);
   remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
 }
