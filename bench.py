@@ -114,12 +114,12 @@ def byte_models(ctx, nnzT):
     tT = 8 * nnzT + 4 * W * nbar            # T values + shared column pattern
     return {
         # per-slice PCG (I4): p = z + beta p, q = A z + beta q, p.q   (reads z p q, writes p q)
-        "void bbot::k_pcg_pq<bbot::EdgeLapView>": 40 * n + om,
+        "void bbot::k_pcg_pq<bbot::LapView>": 40 * n + om,
         "bbot::k_pcg_xr": 48 * n,                      # x += a p, r -= a q, r.r
         "bbot::k_pcg_rz": 16 * n,
-        "void bbot::k_spmv<bbot::EdgeLapView>": 16 * n + om,
-        "void bbot::k_down<bbot::EdgeLapView>": 32 * n + om,
-        "void bbot::k_up<bbot::EdgeLapView>": 36 * n + 8 * nc1A + om,
+        "void bbot::k_spmv<bbot::LapView>": 16 * n + om,
+        "void bbot::k_down<bbot::LapView>": 32 * n + om,
+        "void bbot::k_up<bbot::LapView>": 36 * n + 8 * nc1A + om,
         "void bbot::k_spmv<bbot::SliceEllView>": tT + 16 * m,
         "void bbot::k_down<bbot::SliceEllView>": tT + 32 * m,
         "void bbot::k_up<bbot::SliceEllView>": tT + 36 * m + 8 * nc1T,

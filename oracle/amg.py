@@ -13,12 +13,19 @@ Definition (both sides):
     mutual-maximum matching always progresses on nonsymmetric T).
   * pairwise matching, 16 synchronous rounds: every free row i with
     M_i = max_j s_ij (over free j) > 1e-10 |a_ii| proposes
-    p(i) = min{ j : s_ij >= (1 - tau) M_i }   (tau = 1e-8: near-ties -> lower index);
-    i and j pair iff p(i) = j and p(j) = i.  Leftovers are singletons.
-  * coarse numbering: aggregates ordered by their smallest member.
-  * two matching passes per level (pass 2 on the Galerkin matrix of pass 1),
-    so aggregates have <= 4 rows; prolongation piecewise constant; coarse
-    matrix Galerkin  A_c = P^T A P.
+    p(i) = argmin_prio{ j free : s_ij >= (1 - tau) M_i }   (tau = 1e-8; prio(j) =
+    (lowbias32 hash of j, j): near-ties are broken by a fixed pseudo-random
+    priority so that uniform-weight graphs match in parallel, not along chains);
+    i and j pair iff p(i) = j and p(j) = i.
+  * attach: a row still free with M'_i = max_j s_ij over MATCHED j > 1e-10 |a_ii|
+    joins the pair of t(i) = argmin_prio{ j matched : s_ij >= (1 - tau) M'_i }; other
+    leftovers are singletons.  (Without it, maximal matchings on the dense coarse
+    graphs leave most rows single and coarsening stalls: C3/C4 coarsest blocks of
+    100-400 rows per slice.)
+  * coarse numbering: aggregates ordered by their smallest member (a pair's
+    leader is its smaller row; attached rows take their pair's index).
+  * two matching passes per level (pass 2 on the Galerkin matrix of pass 1);
+    prolongation piecewise constant; coarse matrix Galerkin  A_c = P^T A P.
   * stop: mode "A": max rows per slice <= coarse_max (64); mode "T": total rows
     <= coarse_max (1024); or no coarsening (n_c > 0.9 n); or max_levels.
   * smoother: damped Jacobi (omega), V(1,1) from a zero initial guess.
@@ -34,6 +41,21 @@ import scipy.sparse as sp
 
 TAU = 1e-8
 DECOUPLED = 1e-10
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def prio(j):
+    """Tie-break priority of row j among near-equal strengths: a fixed 32-bit
+    integer hash (lowbias32), then the index.  Lowest priority wins.  (An index
+    tie-break makes uniform-weight graphs match sequentially, one pair per round
+    along a chain, so 16 rounds leave most rows unmatched.)"""
+    x = np.asarray(j, dtype=np.uint64) & _M32
+    x = x ^ (x >> np.uint64(16))
+    x = (x * np.uint64(0x7FEB352D)) & _M32
+    x = x ^ (x >> np.uint64(15))
+    x = (x * np.uint64(0x846CA68B)) & _M32
+    x = x ^ (x >> np.uint64(16))
+    return (x << np.uint64(32)) | (np.asarray(j, dtype=np.uint64) & _M32)
 
 
 def _row_of_nnz(A: sp.csr_matrix):
@@ -55,6 +77,7 @@ def match(A: sp.csr_matrix, slice_of_row: np.ndarray, rounds: int = 16):
     cols = S.indices
     s = S.data
     coupled = np.ones(cols.size, dtype=bool)
+    pc = prio(cols)
     partner = np.full(n, -1, dtype=np.int64)
     free = np.ones(n, dtype=bool)
     for _ in range(rounds):
@@ -64,15 +87,31 @@ def match(A: sp.csr_matrix, slice_of_row: np.ndarray, rounds: int = 16):
         np.maximum.at(Mrow, rows, sv)
         has = free & (Mrow > DECOUPLED * diag)
         cand = ok & has[rows] & (s >= (1.0 - TAU) * Mrow[rows])
-        prop = np.full(n, np.iinfo(np.int64).max, dtype=np.int64)
-        np.minimum.at(prop, rows[cand], cols[cand])
-        prop[~has] = -1
+        best = np.full(n, np.iinfo(np.uint64).max, dtype=np.uint64)
+        np.minimum.at(best, rows[cand], pc[cand])
+        prop = np.where(has, (best & _M32).astype(np.int64), -1)
         i = np.nonzero(prop >= 0)[0]
         mutual = i[prop[prop[i]] == i]
         partner[mutual] = prop[mutual]
         free[mutual] = False
-    leader = np.where(partner >= 0, np.minimum(np.arange(n), partner), np.arange(n))
-    is_leader = leader == np.arange(n)
+    # attach step: a row left unmatched joins the pair of its strongest MATCHED
+    # neighbour (near-ties -> lower index), so every coupled row ends in an
+    # aggregate of >= 2 rows and coarsening cannot stall on dense coarse graphs
+    idx = np.arange(n)
+    pair_leader = np.where(partner >= 0, np.minimum(idx, partner), idx)
+    okm = free[rows] & (partner[cols] >= 0)
+    sv = np.where(okm, s, -np.inf)
+    Mm = np.full(n, -np.inf)
+    np.maximum.at(Mm, rows, sv)
+    hasm = free & (Mm > DECOUPLED * diag)
+    cand = okm & hasm[rows] & (s >= (1.0 - TAU) * Mm[rows])
+    tb = np.full(n, np.iinfo(np.uint64).max, dtype=np.uint64)
+    np.minimum.at(tb, rows[cand], pc[cand])
+    tgt = (tb & _M32).astype(np.int64)
+    leader = pair_leader.copy()
+    att = np.nonzero(hasm)[0]
+    leader[att] = pair_leader[tgt[att]]
+    is_leader = leader == idx
     cidx = np.cumsum(is_leader) - 1
     agg = cidx[leader]
     nc = int(is_leader.sum())

@@ -12,7 +12,7 @@ namespace bbot {
 constexpr double AMG_TAU = 1e-8;        // near-tie tolerance (relative)
 constexpr double AMG_DECOUPLED = 1e-10; // rows with max strength <= this*|a_ii| do not propose
 constexpr int MATCH_ROUNDS = 16;
-constexpr int GAL_CAP = 128;            // max distinct columns of a coarse row
+constexpr int GAL_CAP = 256;            // max distinct columns of a coarse row
 constexpr int MAX_LEVELS = 25;
 constexpr int BS = 256;
 
@@ -84,6 +84,17 @@ __global__ void k_fill_i32(long long n, int* a, int v) {
   if (i < n) a[i] = v;
 }
 
+// tie-break priority among near-equal strengths: (lowbias32(j), j), lowest wins
+__device__ __forceinline__ unsigned long long amg_prio(int j) {
+  unsigned x = (unsigned)j;
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return ((unsigned long long)x << 32) | (unsigned)j;
+}
+
 __global__ void k_propose(long long n, const long long* __restrict__ sp, const int* __restrict__ sj,
                           const double* __restrict__ sw, const double* __restrict__ adiag,
                           const int* __restrict__ free_, int* prop) {
@@ -95,12 +106,15 @@ __global__ void k_propose(long long n, const long long* __restrict__ sp, const i
     if (free_[sj[p]]) M = fmax(M, sw[p]);
   if (!(M > AMG_DECOUPLED * adiag[r])) { prop[r] = -1; return; }
   double thr = (1.0 - AMG_TAU) * M;
-  int best = INT_MAX;
+  unsigned long long best = ~0ULL;
   for (long long p = sp[r]; p < sp[r + 1]; p++) {
     int c = sj[p];
-    if (free_[c] && sw[p] >= thr && c < best) best = c;
+    if (free_[c] && sw[p] >= thr) {
+      unsigned long long pc = amg_prio(c);
+      if (pc < best) best = pc;
+    }
   }
-  prop[r] = best;
+  prop[r] = (int)(best & 0xffffffffULL);
 }
 
 __global__ void k_accept(long long n, const int* __restrict__ prop, int* partner, int* free_) {
@@ -113,19 +127,47 @@ __global__ void k_accept(long long n, const int* __restrict__ prop, int* partner
   }
 }
 
-__global__ void k_leader_flag(long long n, const int* __restrict__ partner, int* flag) {
+// Aggregate leader of every row (I3): a pair's smaller row; a row left free
+// joins the pair of its strongest matched neighbour t(i) = min{ j matched :
+// s_ij >= (1 - tau) M'_i }, M'_i = max over matched j, if M'_i > 1e-10 |a_ii|;
+// otherwise it is a singleton.  flag = 1 on leaders.
+__global__ void k_attach(long long n, const long long* __restrict__ sp, const int* __restrict__ sj,
+                         const double* __restrict__ sw, const double* __restrict__ adiag,
+                         const int* __restrict__ partner, int* lead, int* flag) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int p = partner[r];
-  flag[r] = (p < 0 || r < p) ? 1 : 0;
+  long long L = r;
+  if (p >= 0) {
+    L = r < p ? r : p;
+  } else {
+    double M = -1.0;
+    for (long long q = sp[r]; q < sp[r + 1]; q++)
+      if (partner[sj[q]] >= 0) M = fmax(M, sw[q]);
+    if (M > AMG_DECOUPLED * adiag[r]) {
+      double thr = (1.0 - AMG_TAU) * M;
+      unsigned long long bp = ~0ULL;
+      for (long long q = sp[r]; q < sp[r + 1]; q++) {
+        int c = sj[q];
+        if (partner[c] >= 0 && sw[q] >= thr) {
+          unsigned long long pc = amg_prio(c);
+          if (pc < bp) bp = pc;
+        }
+      }
+      int best = (int)(bp & 0xffffffffULL);
+      int pc = partner[best];
+      L = best < pc ? best : pc;
+    }
+  }
+  lead[r] = (int)L;
+  flag[r] = L == r ? 1 : 0;
 }
 
-__global__ void k_make_agg(long long n, const int* __restrict__ partner, const long long* __restrict__ cidx,
+__global__ void k_make_agg(long long n, const int* __restrict__ lead, const long long* __restrict__ cidx,
                            const int* __restrict__ sl, int* agg, int* slc) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
-  int p = partner[r];
-  long long leader = (p < 0) ? r : (r < p ? r : (long long)p);
+  long long leader = lead[r];
   agg[r] = (int)cidx[leader];
   if (leader == r) slc[cidx[r]] = sl[r];
 }
@@ -238,9 +280,11 @@ __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, con
   long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= nc) return;
   double acc = 0.0;
-  for (long long p = mptr[I]; p < mptr[I + 1]; p++) acc += r[midx[p]];
+  for (long long p = mptr[I]; p < mptr[I + 1]; p++) acc += r[midx[p]];   // P^T r, members ascending
   bc[I] = acc;
 }
+
+
 
 template <class V>
 __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
@@ -365,17 +409,15 @@ __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, cons
 // prolongation + post-smoothing back up to level `tail`, separated by
 // __syncthreads() instead of kernel launches.  Arithmetic is the same per row as
 // k_down / k_restrict / k_coarseA_apply / k_up (same operation order).
-constexpr int TAIL_ROWS = 8192;
+constexpr int TAIL_ROWS = 1024;
 constexpr int TAIL_MAXL = 24;
 constexpr int TAIL_BS = 1024;
 
 struct TailLevel {
-  const long long* rp;
-  const int* ci;
-  const double* v;
+  SellView A;
   const double* dinv;
   double *b, *x, *r, *xo;      // xo: level output (xt, or x at the coarsest)
-  const long long* mptr;       // coarse row -> members (restriction to the next level)
+  const long long* mptr;       // members of the next level's rows (restriction)
   const int* midx;
   const int* agg;
   const long long* sptr;       // device slice pointers
@@ -411,12 +453,19 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
   for (int q = 0; q < nl; q++) {
     const TailLevel& L = T.lv[q];
     long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
+#ifdef BBOT_DEBUG_BOUNDS
+    if (tid == 0 && (s1 > L.A.nrows || s0 < 0)) printf("tail q=%d k=%d s0=%lld s1=%lld n=%lld\n", q, k, s0, s1, L.A.nrows);
+#endif
     for (long long r = s0 + tid; r < s1; r += bs) {
       double acc = L.b[r];
-      for (long long p = L.rp[r]; p < L.rp[r + 1]; p++) {
-        int c = L.ci[p];
-        acc -= L.v[p] * (om * L.dinv[c] * L.b[c]);
-      }
+#ifdef BBOT_DEBUG_BOUNDS
+      L.A.row(r, [&](long long c, double a) {
+        if (c < 0 || c >= L.A.nrows) { printf("tail q=%d r=%lld c=%lld n=%lld\n", q, r, c, L.A.nrows); c = r; }
+        acc -= a * (om * L.dinv[c] * L.b[c]);
+      });
+#else
+      L.A.row(r, [&](long long c, double a) { acc -= a * (om * L.dinv[c] * L.b[c]); });
+#endif
       L.x[r] = om * L.dinv[r] * L.b[r];
       L.r[r] = acc;
     }
@@ -437,6 +486,9 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
     const TailLevel& C = T.lv[nl];
     long long s0 = C.sptr[k];
     int nloc = (int)(C.sptr[k + 1] - s0);
+#ifdef BBOT_DEBUG_BOUNDS
+    if (tid == 0 && (nloc > 128 || nloc > T.cm + 1)) printf("tail coarse k=%d nloc=%d cm=%d\n", k, nloc, T.cm);
+#endif
     const double* inv = T.cinv + (size_t)k * T.cm * T.cm;
     for (int j = tid; j < nloc; j += bs) {
       double acc = 0.0;
@@ -461,10 +513,7 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
     long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
     for (long long r = s0 + tid; r < s1; r += bs) {
       double acc = L.b[r];
-      for (long long p = L.rp[r]; p < L.rp[r + 1]; p++) {
-        int c = L.ci[p];
-        acc -= L.v[p] * (L.x[c] + xc[L.agg[c]]);
-      }
+      L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
       L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
     }
     __syncthreads();
@@ -588,6 +637,35 @@ __global__ void k_view_fill(V v, const long long* __restrict__ rp, int* ci, doub
   v.row(r, [&](long long c, double a) { ci[p] = (int)c; cv[p] = a; p++; });
 }
 
+// ------------------------------------------------------------ CSR -> SELL-32
+__global__ void k_sell_width(long long n, const long long* __restrict__ rp, int* w, long long* w32) {
+  long long ch = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long nch = (n + 31) >> 5;
+  if (ch >= nch) return;
+  int mx = 0;
+  for (long long r = ch * 32; r < n && r < ch * 32 + 32; r++) mx = max(mx, (int)(rp[r + 1] - rp[r]));
+  w[ch] = mx;
+  w32[ch] = 32LL * mx;
+}
+__global__ void k_sell_fill(long long n, const long long* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const long long* __restrict__ off,
+                            const int* __restrict__ w, int* sci, double* sv) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  long long ch = r >> 5;
+  long long base = off[ch] + (r & 31);
+  int len = (int)(rp[r + 1] - rp[r]);
+  for (int s = 0; s < w[ch]; s++) {
+    if (s < len) {
+      sci[base + (long long)s * 32] = ci[rp[r] + s];
+      sv[base + (long long)s * 32] = v[rp[r] + s];
+    } else {
+      sci[base + (long long)s * 32] = (int)r;     // padding: own row, value 0
+      sv[base + (long long)s * 32] = 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------------------ host drivers
 namespace {
 
@@ -631,13 +709,14 @@ void match_pass(Dev& d, const V& v, const int* sl, AmgWork& w, Sg& sg, DBuf<int>
            (const double*)sg.sws.p, (const double*)sg.adiag.p, (const int*)w.free_.p, w.prop.p);
     launch(d, k_accept, dim3(nb), dim3(BS), 0, n, (const int*)w.prop.p, w.partner.p, w.free_.p);
   }
-  launch(d, k_leader_flag, dim3(nb), dim3(BS), 0, n, (const int*)w.partner.p, w.flag.p);
+  launch(d, k_attach, dim3(nb), dim3(BS), 0, n, (const long long*)sg.sp.p, (const int*)sg.sj.p,
+         (const double*)sg.sws.p, (const double*)sg.adiag.p, (const int*)w.partner.p, w.prop.p, w.flag.p);
   grow(w.cidx, n + 1, s);
   exclusive_scan_i32(d, w.flag.p, w.cidx.p, n, w.ws);
   nc = read_scalar(d, w.cidx.p + n);
   agg.alloc(n, s);
   slc.alloc(std::max(1LL, nc), s);
-  launch(d, k_make_agg, dim3(nb), dim3(BS), 0, n, (const int*)w.partner.p, (const long long*)w.cidx.p, sl,
+  launch(d, k_make_agg, dim3(nb), dim3(BS), 0, n, (const int*)w.prop.p, (const long long*)w.cidx.p, sl,
          agg.p, slc.p);
 }
 
@@ -675,6 +754,22 @@ void galerkin(Dev& d, const V& v, long long nc, const long long* mptr, const int
   launch(d, k_galerkin<V, true>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, agg, (int*)nullptr,
          (const long long*)out.rp.p, out.ci.p, out.v.p, w.err.p);
   out.n = nc;
+}
+
+void build_sell(Dev& d, AmgLevel& L, AmgWork& w) {
+  cudaStream_t s = d.stream;
+  long long n = L.n, nch = (n + 31) >> 5;
+  L.sl_w.alloc(std::max(1LL, nch), s);
+  DBuf<long long> w32;
+  w32.alloc(std::max(1LL, nch), s);
+  L.sl_off.alloc(nch + 1, s);
+  launch(d, k_sell_width, dim3(nblocks(nch, BS)), dim3(BS), 0, n, (const long long*)L.rp.p, L.sl_w.p, w32.p);
+  exclusive_scan(d, w32.p, L.sl_off.p, nch, w.ws);
+  long long tot = read_scalar(d, L.sl_off.p + nch);
+  L.sl_ci.alloc(std::max(1LL, tot), s);
+  L.sl_v.alloc(std::max(1LL, tot), s);
+  launch(d, k_sell_fill, dim3(nblocks(n, BS)), dim3(BS), 0, n, (const long long*)L.rp.p, (const int*)L.ci.p,
+         (const double*)L.v.p, (const long long*)L.sl_off.p, (const int*)L.sl_w.p, L.sl_ci.p, L.sl_v.p);
 }
 
 std::vector<long long> slice_ptrs(Dev& d, const int* sl, long long n, int nslices, AmgWork& w) {
@@ -812,6 +907,7 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     d.launches++;
     sync(d);
   }
+  for (size_t l = 1; l < H.lv.size(); l++) build_sell(d, H.lv[l], w);
   // mode A: the per-slice tail starts at the first coarse level with <= TAIL_ROWS rows per slice
   H.tail = 0;
   if (mode == 0 && H.lv.size() >= 2) {
@@ -864,9 +960,7 @@ static void tail_args(AmgHierarchy& H, TailArgs& T) {
   for (int l = H.tail; l < L; l++) {
     AmgLevel& A = H.lv[l];
     TailLevel& t = T.lv[l - H.tail];
-    t.rp = A.rp.p;
-    t.ci = A.ci.p;
-    t.v = A.v.p;
+    t.A = A.sell();
     t.dinv = A.dinv.p;
     t.b = A.b.p;
     t.x = A.x.p;
@@ -892,7 +986,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p);
     else
-      launch(d, k_down<CsrView>, dim3(nb), dim3(BS), 0, lv.view(), (const double*)lv.dinv.p,
+      launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, lv.x.p, lv.r.p);
     if (!(H.mode == 0 && H.tail > 0 && l == stop - 1))
       launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
@@ -917,18 +1011,18 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
              (const int*)lv.agg.p, xc, out);
     } else {
-      launch(d, k_up<CsrView>, dim3(nb), dim3(BS), 0, lv.view(), (const double*)lv.dinv.p,
+      launch(d, k_up<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p, xc, out);
     }
   }
   return fuse != nullptr;
 }
 
-template void amg_setup<EdgeLapView>(Dev&, AmgHierarchy&, const EdgeLapView&, const int*, int, int, double, int,
+template void amg_setup<LapView>(Dev&, AmgHierarchy&, const LapView&, const int*, int, int, double, int,
                                      AmgWork&);
 template void amg_setup<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const int*, int, int, double, int,
                                       AmgWork&);
-template bool amg_vcycle<EdgeLapView>(Dev&, AmgHierarchy&, const EdgeLapView&, const double*, double*,
+template bool amg_vcycle<LapView>(Dev&, AmgHierarchy&, const LapView&, const double*, double*,
                                       const SliceDotFuse*);
 template bool amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*,
                                        const SliceDotFuse*);

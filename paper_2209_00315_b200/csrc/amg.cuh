@@ -17,27 +17,30 @@
 
 namespace bbot {
 
-// rows r = kk*N + f;  A_k = E diag(omega_k) E^T
-struct EdgeLapView {
-  int N, NE;
+// rows r = kk*N + f;  A_k = E diag(omega_k) E^T, stored per cell
+// ("cell-ELL"): off[(kk*4 + t)*N + f] = -omega of the t-th edge of kite f (0 pad),
+// neighbour nb[t*N + f] (-1 pad, shared by all slices).  Slot-major, so a warp
+// reads 32 consecutive doubles per slot; the diagonal is recomputed as the sum
+// of the edge weights in slot order (no separate array).
+struct LapView {
+  int N;
   long long nrows;
-  const int* fe;        // [4][N] fine edge ids (-1 pad)
-  const int* fnb;       // [4][N] neighbours
-  const double* om;     // [K+1][NE]
+  const int* nb;        // [4][N]
+  const double* off;    // [K+1][4][N]
   template <class F>
   __device__ __forceinline__ void row(long long r, F&& f) const {
     int kk = (int)(r / N);
     int fc = (int)(r - (long long)kk * N);
-    const double* w = om + (size_t)kk * NE;
+    const double* o = off + (size_t)kk * 4 * N + fc;
     long long base = (long long)kk * N;
     double d = 0.0;
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      int e = fe[t * N + fc];
-      if (e >= 0) {
-        double o = w[e];
-        d += o;
-        f(base + fnb[t * N + fc], -o);
+      int c = nb[t * N + fc];
+      if (c >= 0) {
+        double a = o[(size_t)t * N];
+        d -= a;
+        f(base + c, a);
       }
     }
     f(r, d);
@@ -45,7 +48,8 @@ struct EdgeLapView {
 };
 
 // rows r = k0*nbar + i; T values tv[((k0*3 + d)*W + s)*nbar + i], column
-// (k0+d-1)*nbar + tcol[s*nbar + i]
+// (k0+d-1)*nbar + tcol[s*nbar + i]; unused slots (tcol = -1) hold exactly 0 and
+// are read as column i (adds an exact 0; no data-dependent loop exit)
 struct SliceEllView {
   int nbar, K, W;
   long long nrows;
@@ -59,10 +63,10 @@ struct SliceEllView {
       int kk = k0 + d - 1;
       if (kk < 0 || kk >= K) continue;
       const double* vv = tv + ((size_t)(k0 * 3 + d) * W) * nbar + i;
+#pragma unroll 4
       for (int s = 0; s < W; s++) {
         int c = tcol[(size_t)s * nbar + i];
-        if (c < 0) break;
-        f((long long)kk * nbar + c, vv[(size_t)s * nbar]);
+        f((long long)kk * nbar + (c < 0 ? i : c), vv[(size_t)s * nbar]);
       }
     }
   }
@@ -76,6 +80,28 @@ struct CsrView {
   template <class F>
   __device__ __forceinline__ void row(long long r, F&& f) const {
     for (long long p = rp[r]; p < rp[r + 1]; p++) f((long long)ci[p], v[p]);
+  }
+};
+
+// SELL-32: rows in chunks of 32; chunk c holds w[c] slots of 32 entries
+// (slot-major: entry s of row r at off[c] + s*32 + (r & 31)), columns in CSR
+// order, padded with (column r, value 0) so the slot loop has no data-dependent
+// exit and its loads issue back to back (a padded term adds an exact 0).  A
+// warp reads one 256-byte segment per slot.  Used by the V-cycle sweeps of the
+// coarse levels; setup keeps the CSR.
+struct SellView {
+  long long nrows;
+  const long long* off;
+  const int* w;
+  const int* ci;
+  const double* v;
+  template <class F>
+  __device__ __forceinline__ void row(long long r, F&& f) const {
+    long long ch = r >> 5;
+    long long base = off[ch] + (r & 31);
+    int wc = w[ch];
+#pragma unroll 4
+    for (int s = 0; s < wc; s++) f((long long)ci[base + (long long)s * 32], v[base + (long long)s * 32]);
   }
 };
 
@@ -93,6 +119,10 @@ struct AmgLevel {
   DBuf<double> b, x, r, xt;      // x: pre-smoothed iterate; xt: this level's V-cycle output
   std::vector<long long> sptr;   // host slice pointers
   DBuf<long long> dsptr;         // the same on the device (per-slice coarse tail)
+  DBuf<long long> sl_off;        // SELL-32 copy of the CSR (V-cycle sweeps)
+  DBuf<int> sl_w, sl_ci;
+  DBuf<double> sl_v;
+  SellView sell() const { return SellView{n, sl_off.p, sl_w.p, sl_ci.p, sl_v.p}; }
   CsrView view() const { return CsrView{n, rp.p, ci.p, v.p}; }
 };
 

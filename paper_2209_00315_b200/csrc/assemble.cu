@@ -173,9 +173,7 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
   BB_CUDA(cudaStreamSynchronize(s));
 }
 
-EdgeLapView view_A(bbot_ctx* c) {
-  return EdgeLapView{c->g.N, c->g.NE, c->n(), c->g.fadj_e.p, c->g.fadj_nb.p, c->as.omega.p};
-}
+LapView view_A(bbot_ctx* c) { return LapView{c->g.N, c->n(), c->g.fadj_nb.p, c->as.Aoff.p}; }
 SliceEllView view_T(bbot_ctx* c) {
   return SliceEllView{c->g.nbar, c->g.K, c->g.W, c->m(), c->g.tcol.p, c->as.Tv.p};
 }
@@ -198,6 +196,22 @@ __global__ void k_edges(int K, int N, int NE, int nbar, const int* __restrict__ 
   double wl = w_len[e];
   omega[t] = e_len[e] * rt / wl;
   gphi[t] = (phi[(size_t)kk * N + L] - phi[(size_t)kk * N + R]) / wl;
+}
+
+// A_k in cell-ELL: Aoff[kk][t][f] = -omega^k of the t-th edge of kite f (0 pad)
+__global__ void k_cell_lap(long long n, int N, int NE, const int* __restrict__ fe, const double* __restrict__ omega,
+                           double* __restrict__ Aoff) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int kk = (int)(r / N);
+  int f = (int)(r - (long long)kk * N);
+  const double* om = omega + (size_t)kk * NE;
+  double* o = Aoff + (size_t)kk * 4 * N + f;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    int e = fe[t * N + f];
+    o[(size_t)t * N] = e >= 0 ? -om[e] : 0.0;
+  }
 }
 
 __global__ void k_coarse_edges(int K, int NEbar, int nbar, const int* __restrict__ ebL, const int* __restrict__ ebR,
@@ -230,6 +244,7 @@ void assemble_edges(bbot_ctx* c) {
   if (A.omega.n != (size_t)ne) {
     A.omega.alloc(ne, s);
     A.gphi.alloc(ne, s);
+    A.Aoff.alloc((size_t)4 * c->n(), s);
     A.omegabar.alloc((size_t)g.K * g.NEbar, s);
     A.Cd.alloc(c->m(), s);
     A.sr.alloc(c->m(), s);
@@ -237,6 +252,8 @@ void assemble_edges(bbot_ctx* c) {
   launch(c->dev, k_edges, dim3(nblocks(ne, BS)), dim3(BS), 0, g.K, g.N, g.NE, g.nbar, (const int*)g.eL.p,
          (const int*)g.eR.p, (const double*)g.lam.p, (const double*)g.e_len.p, (const double*)g.w_len.p,
          (const double*)c->phi.p, (const double*)c->rho_ext.p, A.omega.p, A.gphi.p);
+  launch(c->dev, k_cell_lap, dim3(nblocks(c->n(), BS)), dim3(BS), 0, c->n(), g.N, g.NE, (const int*)g.fadj_e.p,
+         (const double*)A.omega.p, A.Aoff.p);
   long long nce = (long long)g.K * g.NEbar;
   launch(c->dev, k_coarse_edges, dim3(nblocks(nce, BS)), dim3(BS), 0, g.K, g.NEbar, g.nbar, (const int*)g.ebL.p,
          (const int*)g.ebR.p, (const double*)g.lam_bar.p, (const double*)g.ebar_coef.p,

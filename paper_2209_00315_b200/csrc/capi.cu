@@ -95,9 +95,17 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
     c->dev.stream = (cudaStream_t)stream;
     int devid = 0;
     BB_CUDA(cudaGetDevice(&devid));
+    {   // keep freed stream-ordered memory in the pool: the AMG hierarchies are rebuilt every
+        // Newton step, and a release threshold of 0 would unmap/remap them at every sync
+      cudaMemPool_t pool;
+      BB_CUDA(cudaDeviceGetDefaultMemPool(&pool, devid));
+      unsigned long long thr = ~0ULL;
+      BB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     BB_CUDA(cudaDeviceGetAttribute(&c->dev.num_sms, cudaDevAttrMultiProcessorCount, devid));
     c->red.init(&c->dev, std::max(K + 2, 64));
     if (const char* e = getenv("BBOT_EAGER")) c->use_graph = (atoi(e) == 0);
+    if (const char* e = getenv("BBOT_SYNC_CHECK")) c->dev.sync_check = (atoi(e) != 0);
     for (int i = 0; i < nt; i++)
       BB_REQUIRE(rho_in[i] >= 0 && rho_f[i] >= 0 && std::isfinite(rho_in[i]) && std::isfinite(rho_f[i]),
                  BBOT_E_INPUT, "densities must be finite and >= 0");

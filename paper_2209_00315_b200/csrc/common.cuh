@@ -49,6 +49,7 @@ struct Dev {
   int num_sms = 148;
   bool prof = false;
   bool capturing = false;      // kernels are being captured into a CUDA graph
+  bool sync_check = false;     // BBOT_SYNC_CHECK=1: synchronise after every eager launch (debug)
   int depth = 0;               // nesting depth of device loops being captured
   std::vector<cudaStream_t> cap_streams;
   std::vector<ProfRec> recs;
@@ -84,8 +85,12 @@ inline void launch(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, Args...
   }
   if (!d.capturing) d.launches++;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess)
-    throw Error(BBOT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (e == cudaSuccess && d.sync_check && !d.capturing) e = cudaStreamSynchronize(d.stream);
+  if (e != cudaSuccess) {
+    const char* nm = nullptr;
+    cudaFuncGetName(&nm, (const void*)kernel);
+    throw Error(BBOT_E_CUDA, std::string("kernel ") + (nm ? nm : "?") + ": " + cudaGetErrorString(e));
+  }
 }
 
 inline unsigned nblocks(long long n, int bs, long long cap = 1LL << 30) {
@@ -288,15 +293,16 @@ struct Reducer {
   void init(Dev* d, int max_slices) {
     dev = d;
     // (parts <= 1024) x (<= 33 CGS2 dots) covers every multi-result reduction
-    cap = std::max((size_t)8 * d->num_sms + 2 * (size_t)max_slices + 4096, (size_t)1024 * 33);
+    cap = std::max((size_t)16 * d->num_sms + 2 * (size_t)max_slices + 4096, (size_t)1024 * 33);
     partial.alloc(cap, d->stream);
     counter.alloc(1, d->stream);
     counter.zero();
   }
-  // blocks per slice: ~2048 elements per block, <= 8 blocks per SM in total
+  // blocks per slice: ~512 elements per block (2 per thread: enough loads in
+  // flight), <= 16 blocks per SM in total
   int parts_for(long long len, int nslices) const {
-    long long p = (len + 2047) / 2048;
-    long long cap_b = std::max(1LL, (long long)(8 * dev->num_sms) / std::max(1, nslices));
+    long long p = (len + 511) / 512;
+    long long cap_b = std::max(1LL, (long long)(16 * dev->num_sms) / std::max(1, nslices));
     p = std::min(p, cap_b);
     p = std::min(p, 1024LL);
     return (int)std::max(1LL, p);

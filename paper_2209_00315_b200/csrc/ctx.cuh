@@ -54,6 +54,7 @@ struct DevGeom {
 struct Assembled {
   bool valid = false;
   DBuf<double> omega, gphi;       // [K+1][NE]
+  DBuf<double> Aoff;              // [K+1][4][N] A_k off-diagonals per kite slot (cell-ELL, -omega)
   DBuf<double> omegabar;          // [K][NEbar]
   DBuf<double> Cd, sr;            // C = cbar s/rho, s/rho  (m)
   DBuf<double> f, g, h, gt;       // RHS pieces

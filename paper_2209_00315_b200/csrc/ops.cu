@@ -113,21 +113,20 @@ static BtRow make_btrow(bbot_ctx* c) {
 }
 
 // ---------------------------------------------------------------- a2: J_P
-__global__ void k_jp_y1(long long n, int N, int NE, const double* __restrict__ omega, const int* __restrict__ fe,
-                        const int* __restrict__ fnb, BtRow bt, const double* __restrict__ x1,
-                        const double* __restrict__ x2, const double* __restrict__ S, double inv_area,
-                        double* __restrict__ y1) {
+__global__ void k_jp_y1(long long n, int N, const double* __restrict__ Aoff, const int* __restrict__ fnb, BtRow bt,
+                        const double* __restrict__ x1, const double* __restrict__ x2, const double* __restrict__ S,
+                        double inv_area, double* __restrict__ y1) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   int kk = (int)(t / N);
   long long f = t - (long long)kk * N;
   const double* xs = x1 + (size_t)kk * N;
-  const double* om = omega + (size_t)kk * NE;
+  const double* o = Aoff + (size_t)kk * 4 * N + f;
   double xf = xs[f], acc = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    int e = fe[q * N + f];
-    if (e >= 0) acc += om[e] * (xf - xs[fnb[q * N + f]]);
+    int c = fnb[q * N + f];
+    if (c >= 0) acc -= o[(size_t)q * N] * (xf - xs[c]);     // omega_e (x_f - x_c), A_k x
   }
   y1[t] = acc + bt(x2, S, inv_area, kk, f);     // A x1 + B^T P^T x2
 }
@@ -156,8 +155,8 @@ void jp_matvec(bbot_ctx* c, const double* x, double* y) {
   double* S1 = c->scal.p;            // c-bar weighted slice sums of x2 (P^T)
   double* S2 = c->scal.p + (K + 2);  // plain slice sums of t (P)
   c->red.slice_sum(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, K, S1, false);
-  launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, g.NE, (const double*)c->as.omega.p,
-         (const int*)g.fadj_e.p, (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
+  launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)c->as.Aoff.p,
+         (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
          1.0 / g.area, y);
   c->red.slice_sum(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, K, S2, false);
   launch(c->dev, k_sub_slice_w, dim3(nblocks(m, BS)), dim3(BS), 0, (long long)g.nbar, K, y + n,
@@ -179,8 +178,8 @@ void apply_T(bbot_ctx* c, const double* x, double* y) {
   launch(c->dev, k_spmv<SliceEllView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
 }
 void apply_A(bbot_ctx* c, const double* x, double* y) {
-  EdgeLapView v = view_A(c);
-  launch(c->dev, k_spmv<EdgeLapView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
+  LapView v = view_A(c);
+  launch(c->dev, k_spmv<LapView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
 }
 
 // ---------------------------------------------------------------- a4 pieces

@@ -10,7 +10,7 @@ void upload_geometry(bbot_ctx* c, const Geometry& g, int K);
 void assemble_edges(bbot_ctx* c);                    // omega, gphi, omegabar, C, s/rho
 void compute_residual(bbot_ctx* c, bool write_rhs);  // F (as f,g,h = -F), g~, rhs, norms
 void assemble_T(bbot_ctx* c);                        // T values
-EdgeLapView view_A(bbot_ctx* c);
+LapView view_A(bbot_ctx* c);
 SliceEllView view_T(bbot_ctx* c);
 
 // ops.cu

@@ -96,7 +96,7 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   // (iii) b = r1 - B^T P^T y, slice means removed (compatibility)
   bb_rhs_A(c, r1, z2, c->tmp_n2.p);
   // (iv) A_k x^k = b^k: per-slice PCG + AMG(A) V-cycle (4.20), then slice means removed
-  EdgeLapView vA = view_A(c);
+  LapView vA = view_A(c);
   c->pcg.emit(
       c->dev, c->red, vA,
       [&](const double* x, double* y, const SliceDotFuse* f) { return amg_vcycle(c->dev, c->amgA, vA, x, y, f); },

@@ -62,23 +62,34 @@ def _lap1d(n):
 
 
 def test_matching_and_galerkin():
-    """Pairs are mutual, within a slice, aggregates <= 4 rows after 2 passes,
-    coarse = P^T A P (brute force dense)."""
+    """I3: pairs are mutual and within a slice; every coupled row
+    ends in an aggregate of >= 2 rows (attach step); coarse = P^T A P (brute
+    force dense); tie-breaking and the attach rule on hand-worked cases."""
     A = sp.block_diag([_lap1d(37), _lap1d(23)], format="csr")
     sl = np.r_[np.zeros(37, int), np.ones(23, int)]
     agg, nc, slc = amg.match(A, sl)
-    assert np.all(np.bincount(agg) <= 2)
+    sizes = np.bincount(agg)
+    assert np.all(sizes >= 2) and np.all(sizes <= 4)
     for c in range(nc):
         mem = np.nonzero(agg == c)[0]
         assert len(set(sl[mem])) == 1
+        assert np.all(np.diff(mem) == 1)          # 1-D: aggregates are contiguous runs
     H = amg.setup(A, sl, "A", 2 / 3, coarse_max=4)
-    assert np.all(np.bincount(H.levels[0].agg) <= 4)
     P = np.zeros((60, H.levels[0].nc))
     P[np.arange(60), H.levels[0].agg] = 1
     assert np.allclose(H.levels[1].A.toarray(), P.T @ A.toarray() @ P, atol=1e-14)
-    # uniform weights: ties are broken towards the lower index -> (0,1),(2,3),... on level 1
-    agg1, _, _ = amg.match(_lap1d(8), np.zeros(8, int))
-    assert list(agg1) == [0, 0, 1, 1, 2, 2, 3, 3]
+    # uniform weights: near-ties go to the lowest prio(j) (hash, then index).
+    # 1-D, 5 rows, prio order 0 < 3 < 1 < 2 < 4: round 1: 0 -> 1, 1 -> 0 (mutual),
+    # 2 -> 3 (prio 3 < 1), 3 -> 2 (prio 2 < 4) (mutual), 4 -> 3; row 4 is left free
+    # and joins the pair of its only matched neighbour 3 -> aggregates {0,1},{2,3,4}
+    hp = [int(v) >> 32 for v in amg.prio(np.arange(5))]
+    assert sorted(range(5), key=lambda j: hp[j]) == [0, 3, 1, 2, 4]
+    agg5, nc5, _ = amg.match(_lap1d(5), np.zeros(5, int))
+    assert list(agg5) == [0, 0, 1, 1, 1] and nc5 == 2
+    # a decoupled row (zero off-diagonals) stays a singleton
+    D = sp.block_diag([_lap1d(4), sp.csr_matrix([[1.0]])], format="csr")
+    aggD, ncD, _ = amg.match(D, np.zeros(5, int))
+    assert list(aggD) == [0, 0, 1, 1, 2] and ncD == 3
 
 
 def test_vcycle_symmetric_and_convergent():
