@@ -343,7 +343,7 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "no flush; per-step working set (FGMRES basis 61 x (n+m) x 8 B) exceeds the 126 MB L2"},
             "unknowns_per_s": value * (ctx.n + ctx.m),
-            "solve": {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "converged", "rel_res",
+            "solve": {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "inner_A_its_total", "converged", "rel_res",
                                          "amg_levels_A", "amg_levels_T")},
             "e2e": {"value": world * args.steps / te, "unit": "solves/s", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes},

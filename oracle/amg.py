@@ -41,6 +41,11 @@ import scipy.sparse as sp
 
 TAU = 1e-8
 DECOUPLED = 1e-10
+KC_ROWS = 4096      # mode A: K-cycle on coarse levels with <= KC_ROWS rows per slice ...
+KC_MIN_LEVELS = 7   # ... in hierarchies of >= KC_MIN_LEVELS levels.  Plain aggregation
+#                    V-cycles lose level independence: per-slice PCG to 1e-3 needs 29 its on
+#                    C2 (5 levels) but 64 on C4 (8 levels); the K-cycle on the coarse levels
+#                    brings C4 back to ~31, while on the shallow C2 it only costs
 _M32 = np.uint64(0xFFFFFFFF)
 
 
@@ -143,6 +148,8 @@ class Hierarchy:
     omega: float
     coarse_inv: list = field(default_factory=list)   # mode A: per slice (rows, inv of grounded block)
     coarse_dense_inv: np.ndarray | None = None        # mode T
+    nslices: int = 0
+    kcycle: list = field(default_factory=list)       # level l: coarse correction INTO l by the K-cycle
 
     @property
     def sizes(self):
@@ -175,7 +182,10 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
         lv.nc = nc2
         cur = galerkin(A1, agg2, nc2)
         cur_slice = sl2
-    H = Hierarchy(levels=levels, mode=mode, omega=omega)
+    H = Hierarchy(levels=levels, mode=mode, omega=omega, nslices=nslices)
+    L = len(levels)
+    H.kcycle = [mode == "A" and L >= KC_MIN_LEVELS and 0 < l < L - 1 and
+                _slice_sizes(levels[l].slice_of_row, nslices).max() <= KC_ROWS for l in range(L)]
     Ac = levels[-1].A.toarray()
     if mode == "A":
         sl = levels[-1].slice_of_row
@@ -202,8 +212,46 @@ def _coarse_solve(H: Hierarchy, b):
     return x
 
 
+def _sdot(H, level, u, v):
+    """per-slice dot products at a level"""
+    return np.bincount(H.levels[level].slice_of_row, weights=u * v, minlength=H.nslices)
+
+
+def _safe_div(a, b):
+    return np.where(b != 0, a / np.where(b != 0, b, 1.0), 0.0)
+
+
+def kstep(H: Hierarchy, rc, level: int):
+    """K-cycle coarse correction at `level` (Notay & Vassilevski's K-cycle, the
+    acceleration AGMG uses): two flexible-CG steps on A_level e = rc, per time
+    slice, preconditioned by the cycle of `level`, always two steps (no branch):
+        c1 = cyc(rc), v1 = A c1, rho1 = c1.v1, a1 = c1.rc, r2 = rc - (a1/rho1) v1
+        c2 = cyc(r2), v2 = A c2, g = c2.v1, beta = c2.v2, a2 = c2.r2,
+        rho2 = beta - g^2/rho1
+        e = (a1/rho1 - g a2/(rho1 rho2)) c1 + (a2/rho2) c2
+    (x/0 -> 0 on slices with a zero denominator)."""
+    A = H.levels[level].A
+    sl = H.levels[level].slice_of_row
+    c1 = vcycle(H, rc, level)
+    v1 = A @ c1
+    rho1 = _sdot(H, level, c1, v1)
+    a1 = _sdot(H, level, c1, rc)
+    f1 = _safe_div(a1, rho1)
+    r2 = rc - f1[sl] * v1
+    c2 = vcycle(H, r2, level)
+    g = _sdot(H, level, c2, v1)
+    a2 = _sdot(H, level, c2, r2)
+    v2 = A @ c2
+    beta = _sdot(H, level, c2, v2)
+    rho2 = beta - g * _safe_div(g, rho1)
+    g2 = _safe_div(a2, rho2)
+    return (f1 - g * _safe_div(g2, rho1))[sl] * c1 + g2[sl] * c2
+
+
 def vcycle(H: Hierarchy, b, level: int = 0):
-    """One V(1,1) cycle with damped Jacobi, zero initial guess."""
+    """One V(1,1) cycle with damped Jacobi from a zero initial guess; in mode A the
+    coarse correction into a level with <= KC_ROWS rows per slice (not the
+    coarsest) is a K-cycle step (kstep) instead of a single recursive cycle."""
     if level == len(H.levels) - 1:
         return _coarse_solve(H, b)
     lv = H.levels[level]
@@ -211,7 +259,10 @@ def vcycle(H: Hierarchy, b, level: int = 0):
     x = w * lv.dinv * b                                  # pre-smooth from x = 0
     r = b - lv.A @ x
     bc = np.bincount(lv.agg, weights=r, minlength=lv.nc)  # restriction P^T r
-    xc = vcycle(H, bc, level + 1)
+    if H.kcycle and H.kcycle[level + 1]:
+        xc = kstep(H, bc, level + 1)
+    else:
+        xc = vcycle(H, bc, level + 1)
     x = x + xc[lv.agg]                                   # prolongation
     x = x + w * lv.dinv * (b - lv.A @ x)                 # post-smooth
     return x

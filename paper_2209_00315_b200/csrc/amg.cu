@@ -266,9 +266,9 @@ __global__ void k_slice_ptr(long long n, const int* __restrict__ sl, int nslices
 // ------------------------------------------------------------ V-cycle kernels
 template <class V>
 __global__ void k_down(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
-                       double* __restrict__ x, double* __restrict__ res) {
+                       double* __restrict__ x, double* __restrict__ res, SliceSkip sk) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows) return;
+  if (r >= v.nrows || sk.skip(r)) return;
   double acc = b[r];
   v.row(r, [&](long long c, double a) { acc -= a * (om * dinv[c] * b[c]); });
   x[r] = om * dinv[r] * b[r];
@@ -276,9 +276,9 @@ __global__ void k_down(V v, const double* __restrict__ dinv, const double* __res
 }
 
 __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
-                           const double* __restrict__ r, double* bc) {
+                           const double* __restrict__ r, double* bc, SliceSkip sk) {
   long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= nc) return;
+  if (I >= nc || sk.skip(I)) return;
   double acc = 0.0;
   for (long long p = mptr[I]; p < mptr[I + 1]; p++) acc += r[midx[p]];   // P^T r, members ascending
   bc[I] = acc;
@@ -289,9 +289,9 @@ __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, con
 template <class V>
 __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
                      const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
-                     double* __restrict__ xo) {
+                     double* __restrict__ xo, SliceSkip sk) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows) return;
+  if (r >= v.nrows || sk.skip(r)) return;
   double acc = b[r];
   v.row(r, [&](long long c, double a) { acc -= a * (x[c] + xc[agg[c]]); });
   xo[r] = (x[r] + xc[agg[r]]) + om * dinv[r] * acc;
@@ -302,10 +302,11 @@ __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restr
 template <class V>
 __global__ void k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
                          const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
-                         double* __restrict__ xo, long long L, RedArgs R, PcgRzFin fin) {
+                         double* __restrict__ xo, long long L, RedArgs R, PcgRzFin fin, const double* active) {
   int k = blockIdx.y;
   long long beg, end;
   red_chunk(L, R.parts, beg, end);
+  if (active && active[k] == 0.0) end = beg;     // converged slice: nothing to do (partial 0)
   double dot = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     long long r = (long long)k * L + i;
@@ -402,14 +403,15 @@ __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, cons
 }
 
 // ------------------------------------------------------------ per-slice coarse tail (mode A)
-// AMG(A) never aggregates across time slices (I3), so below the level where a
-// slice has <= TAIL_ROWS rows the rest of the V-cycle is independent per slice:
-// one CTA per slice runs restriction from level tail-1, every coarser level's
-// pre-smoothing + residual + restriction, the grounded coarsest solve, and the
-// prolongation + post-smoothing back up to level `tail`, separated by
-// __syncthreads() instead of kernel launches.  Arithmetic is the same per row as
-// k_down / k_restrict / k_coarseA_apply / k_up (same operation order).
-constexpr int TAIL_ROWS = 1024;
+// AMG(A) never aggregates across time slices (I3), so below the first level with
+// <= TAIL_ROWS rows per slice the rest of the cycle is independent per slice:
+// one CTA per slice runs the restriction from level tail-1 and the whole coarse
+// cycle -- damped-Jacobi V(1,1) steps, the K-cycle coarse corrections (two
+// flexible-CG steps with per-slice block reductions, I3/oracle kstep) and the
+// grounded coarsest solve -- separated by __syncthreads() instead of launches.
+// The level table lives in device memory (TailArgs), read through a pointer.
+constexpr int TAIL_ROWS = 4096;      // == oracle KC_ROWS: the tail levels are the K-cycle candidates
+constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
 constexpr int TAIL_MAXL = 24;
 constexpr int TAIL_BS = 1024;
 
@@ -417,10 +419,12 @@ struct TailLevel {
   SellView A;
   const double* dinv;
   double *b, *x, *r, *xo;      // xo: level output (xt, or x at the coarsest)
+  double *kc1, *kv, *krc;      // K-cycle work vectors
   const long long* mptr;       // members of the next level's rows (restriction)
   const int* midx;
   const int* agg;
   const long long* sptr;       // device slice pointers
+  int kc;                      // 1: the coarse correction into this level is a K-cycle step
 };
 struct TailArgs {
   int first, last;             // levels first..last (last = coarsest)
@@ -434,66 +438,76 @@ struct TailArgs {
   TailLevel lv[TAIL_MAXL];
 };
 
-__global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
-  const int k = blockIdx.x;
+// per-slice dot over rows [s0, s1): block reduction, result broadcast to all threads
+__device__ __forceinline__ double tail_dot(const double* u, const double* v, long long s0, long long s1) {
+  __shared__ double res;
+  double acc = 0.0;
+  for (long long r = s0 + threadIdx.x; r < s1; r += blockDim.x) acc += u[r] * v[r];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) res = acc;
+  __syncthreads();
+  double out = res;
+  __syncthreads();
+  return out;
+}
+__device__ __forceinline__ double tail_div(double a, double b) { return b != 0.0 ? a / b : 0.0; }
+
+__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k);
+
+// K-cycle step at tail level q: input lv[q].b (= rc), output lv[q].xo (oracle amg.kstep)
+__device__ void tail_kstep(const TailArgs* __restrict__ T, int q, int k) {
+  const TailLevel& L = T->lv[q];
+  const long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
   const int tid = threadIdx.x, bs = blockDim.x;
-  const double om = T.om;
-  // restriction from level first-1 (rows of slice k at level `first` are contiguous)
-  {
-    const TailLevel& F = T.lv[0];
-    long long s0 = F.sptr[k], s1 = F.sptr[k + 1];
-    for (long long I = s0 + tid; I < s1; I += bs) {
-      double acc = 0.0;
-      for (long long p = T.mptr0[I]; p < T.mptr0[I + 1]; p++) acc += T.r0[T.midx0[p]];
-      F.b[I] = acc;
-    }
+  for (long long r = s0 + tid; r < s1; r += bs) L.krc[r] = L.b[r];
+  __syncthreads();
+  tail_cycle(T, q, k);                                   // c1 -> xo
+  for (long long r = s0 + tid; r < s1; r += bs) {
+    double c = L.xo[r];
+    L.kc1[r] = c;
+    double av = 0.0;
+    L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
+    L.kv[r] = av;                                        // v1 = A c1
   }
   __syncthreads();
-  const int nl = T.last - T.first;     // levels with smoothing (coarsest excluded)
-  for (int q = 0; q < nl; q++) {
-    const TailLevel& L = T.lv[q];
-    long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
-#ifdef BBOT_DEBUG_BOUNDS
-    if (tid == 0 && (s1 > L.A.nrows || s0 < 0)) printf("tail q=%d k=%d s0=%lld s1=%lld n=%lld\n", q, k, s0, s1, L.A.nrows);
-#endif
-    for (long long r = s0 + tid; r < s1; r += bs) {
-      double acc = L.b[r];
-#ifdef BBOT_DEBUG_BOUNDS
-      L.A.row(r, [&](long long c, double a) {
-        if (c < 0 || c >= L.A.nrows) { printf("tail q=%d r=%lld c=%lld n=%lld\n", q, r, c, L.A.nrows); c = r; }
-        acc -= a * (om * L.dinv[c] * L.b[c]);
-      });
-#else
-      L.A.row(r, [&](long long c, double a) { acc -= a * (om * L.dinv[c] * L.b[c]); });
-#endif
-      L.x[r] = om * L.dinv[r] * L.b[r];
-      L.r[r] = acc;
-    }
-    __syncthreads();
-    const TailLevel& C = T.lv[q + 1];
-    long long c0 = C.sptr[k], c1 = C.sptr[k + 1];
-    for (long long I = c0 + tid; I < c1; I += bs) {
-      double acc = 0.0;
-      for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
-      C.b[I] = acc;
-    }
-    __syncthreads();
+  const double rho1 = tail_dot(L.kc1, L.kv, s0, s1);
+  const double a1 = tail_dot(L.kc1, L.krc, s0, s1);
+  const double f1 = tail_div(a1, rho1);
+  for (long long r = s0 + tid; r < s1; r += bs) L.b[r] = L.krc[r] - f1 * L.kv[r];   // r2
+  __syncthreads();
+  tail_cycle(T, q, k);                                   // c2 -> xo
+  const double g = tail_dot(L.xo, L.kv, s0, s1);
+  const double a2 = tail_dot(L.xo, L.b, s0, s1);
+  for (long long r = s0 + tid; r < s1; r += bs) {
+    double av = 0.0;
+    L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
+    L.kv[r] = av;                                        // v2 = A c2
   }
-  // coarsest: grounded at the slice's first row, then the slice mean removed
-  {
+  __syncthreads();
+  const double beta = tail_dot(L.xo, L.kv, s0, s1);
+  const double rho2 = beta - g * tail_div(g, rho1);
+  const double g2 = tail_div(a2, rho2);
+  const double e1 = f1 - g * tail_div(g2, rho1);
+  for (long long r = s0 + tid; r < s1; r += bs) L.xo[r] = e1 * L.kc1[r] + g2 * L.xo[r];
+  __syncthreads();
+}
+
+// cycle of tail level q: input lv[q].b, output lv[q].xo
+__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k) {
+  const int tid = threadIdx.x, bs = blockDim.x;
+  const int nl = T->last - T->first;
+  const double om = T->om;
+  if (q == nl) {   // coarsest: grounded at the slice's first row, then the slice mean removed
     __shared__ double xs[128];
     __shared__ double mean;
-    const TailLevel& C = T.lv[nl];
+    const TailLevel& C = T->lv[nl];
     long long s0 = C.sptr[k];
     int nloc = (int)(C.sptr[k + 1] - s0);
-#ifdef BBOT_DEBUG_BOUNDS
-    if (tid == 0 && (nloc > 128 || nloc > T.cm + 1)) printf("tail coarse k=%d nloc=%d cm=%d\n", k, nloc, T.cm);
-#endif
-    const double* inv = T.cinv + (size_t)k * T.cm * T.cm;
+    const double* inv = T->cinv + (size_t)k * T->cm * T->cm;
     for (int j = tid; j < nloc; j += bs) {
       double acc = 0.0;
       if (j > 0)
-        for (int l = 1; l < nloc; l++) acc += inv[(j - 1) * T.cm + (l - 1)] * C.b[s0 + l];
+        for (int l = 1; l < nloc; l++) acc += inv[(j - 1) * T->cm + (l - 1)] * C.b[s0 + l];
       xs[j] = acc;
     }
     __syncthreads();
@@ -506,18 +520,52 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(TailArgs T) {
     __syncthreads();
     for (int j = tid; j < nloc; j += bs) C.xo[s0 + j] = xs[j] - mean;
     __syncthreads();
+    return;
   }
-  for (int q = nl - 1; q >= 0; q--) {
-    const TailLevel& L = T.lv[q];
-    const double* xc = T.lv[q + 1].xo;
-    long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
-    for (long long r = s0 + tid; r < s1; r += bs) {
-      double acc = L.b[r];
-      L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
-      L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
+  const TailLevel& L = T->lv[q];
+  const long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
+  for (long long r = s0 + tid; r < s1; r += bs) {
+    double acc = L.b[r];
+    L.A.row(r, [&](long long c, double a) { acc -= a * (om * L.dinv[c] * L.b[c]); });
+    L.x[r] = om * L.dinv[r] * L.b[r];
+    L.r[r] = acc;
+  }
+  __syncthreads();
+  const TailLevel& C = T->lv[q + 1];
+  const long long c0 = C.sptr[k], c1 = C.sptr[k + 1];
+  for (long long I = c0 + tid; I < c1; I += bs) {
+    double acc = 0.0;
+    for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
+    C.b[I] = acc;
+  }
+  __syncthreads();
+  if (C.kc) tail_kstep(T, q + 1, k);
+  else tail_cycle(T, q + 1, k);
+  const double* xc = C.xo;
+  for (long long r = s0 + tid; r < s1; r += bs) {
+    double acc = L.b[r];
+    L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
+    L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(TAIL_BS) k_tailA(const TailArgs* __restrict__ T, const double* active) {
+  const int k = blockIdx.x;
+  if (active && active[k] == 0.0) return;        // converged slice
+  const int tid = threadIdx.x, bs = blockDim.x;
+  {   // restriction from level first-1 (rows of slice k at level `first` are contiguous)
+    const TailLevel& F = T->lv[0];
+    long long s0 = F.sptr[k], s1 = F.sptr[k + 1];
+    for (long long I = s0 + tid; I < s1; I += bs) {
+      double acc = 0.0;
+      for (long long p = T->mptr0[I]; p < T->mptr0[I + 1]; p++) acc += T->r0[T->midx0[p]];
+      F.b[I] = acc;
     }
-    __syncthreads();
   }
+  __syncthreads();
+  if (T->lv[0].kc) tail_kstep(T, 0, k);
+  else tail_cycle(T, 0, k);
 }
 
 // mode T: dense Gauss-Jordan in global memory, two launches per pivot
@@ -784,6 +832,8 @@ std::vector<long long> slice_ptrs(Dev& d, const int* sl, long long n, int nslice
 
 }  // namespace
 
+static void tail_args(AmgHierarchy& H, TailArgs& T);
+
 template <class V0>
 void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nslices, int mode, double omega,
                int coarse_max, AmgWork& w) {
@@ -920,13 +970,22 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
         break;
       }
     }
+    static TailArgs hostT;   // staging (the copy below completes before the sync)
     for (int l = std::max(1, H.tail); H.tail > 0 && l < L; l++) {
       AmgLevel& A = H.lv[l];
       A.dsptr.alloc(nslices + 1, s);
       BB_CUDA(cudaMemcpyAsync(A.dsptr.p, A.sptr.data(), (nslices + 1) * sizeof(long long), cudaMemcpyHostToDevice,
                               s));
+      A.kc1.alloc(A.n, s);
+      A.kv.alloc(A.n, s);
+      A.krc.alloc(A.n, s);
     }
-    sync(d);   // the host slice-pointer vectors are sources of the async copies above
+    if (H.tail > 0) {
+      tail_args(H, hostT);
+      H.tail_args.alloc(sizeof(TailArgs), s);
+      BB_CUDA(cudaMemcpyAsync(H.tail_args.p, &hostT, sizeof(TailArgs), cudaMemcpyHostToDevice, s));
+    }
+    sync(d);   // the host slice-pointer vectors / staging are sources of the async copies above
   }
   H.ready = true;
 }
@@ -966,36 +1025,42 @@ static void tail_args(AmgHierarchy& H, TailArgs& T) {
     t.x = A.x.p;
     t.r = A.r.p;
     t.xo = level_out(H, l);
+    t.kc1 = A.kc1.p;
+    t.kv = A.kv.p;
+    t.krc = A.krc.p;
     t.mptr = A.mptr.p;
     t.midx = A.midx.p;
     t.agg = A.agg.p;
     t.sptr = A.dsptr.p;
+    t.kc = (L >= KC_MIN_LEVELS && l < L - 1) ? 1 : 0;   // K-cycle levels (oracle amg.setup kcycle)
   }
 }
 
 template <class V0>
-bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, const SliceDotFuse* fuse) {
+bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, const SliceDotFuse* fuse,
+                const double* active) {
   int L = (int)H.lv.size();
   if (L == 1) { coarse_solve(d, H, b, x); return false; }
   double om = H.omega;
+  if (H.mode != 0) active = nullptr;                // T couples slices: never skip
+  const long long L0 = H.lv[0].n / std::max(1, H.nslices);
+  auto skip_at = [&](int l) { return SliceSkip{active, l == 0 ? nullptr : (const int*)H.lv[l].slice_of.p, L0}; };
   // grid-wide levels: 0 .. stop-1; below: the per-slice tail (mode A) or more grid levels
   int stop = (H.mode == 0 && H.tail > 0) ? H.tail : L - 1;
   for (int l = 0; l < stop; l++) {
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
     if (l == 0)
-      launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p);
+      launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0));
     else
       launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
-             (const double*)lv.b.p, om, lv.x.p, lv.r.p);
+             (const double*)lv.b.p, om, lv.x.p, lv.r.p, skip_at(l));
     if (!(H.mode == 0 && H.tail > 0 && l == stop - 1))
       launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
-             (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p);
+             (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1));
   }
   if (H.mode == 0 && H.tail > 0) {
-    TailArgs T;
-    tail_args(H, T);
-    launch(d, k_tailA, dim3(H.nslices), dim3(TAIL_BS), 0, T);
+    launch(d, k_tailA, dim3(H.nslices), dim3(TAIL_BS), 0, (const TailArgs*)H.tail_args.p, active);
   } else {
     coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
   }
@@ -1006,13 +1071,13 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     const double* xc = level_out(H, l + 1);
     if (l == 0 && fuse) {
       launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
-             (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin);
+             (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
-             (const int*)lv.agg.p, xc, out);
+             (const int*)lv.agg.p, xc, out, skip_at(0));
     } else {
       launch(d, k_up<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
-             (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p, xc, out);
+             (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, skip_at(l));
     }
   }
   return fuse != nullptr;
@@ -1023,8 +1088,8 @@ template void amg_setup<LapView>(Dev&, AmgHierarchy&, const LapView&, const int*
 template void amg_setup<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const int*, int, int, double, int,
                                       AmgWork&);
 template bool amg_vcycle<LapView>(Dev&, AmgHierarchy&, const LapView&, const double*, double*,
-                                      const SliceDotFuse*);
+                                  const SliceDotFuse*, const double*);
 template bool amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*,
-                                       const SliceDotFuse*);
+                                       const SliceDotFuse*, const double*);
 
 }  // namespace bbot

@@ -105,6 +105,20 @@ struct SellView {
   }
 };
 
+// Skip rows of converged time slices (PCG on the block-diagonal A, mode A only):
+// AMG(A) never couples slices, so leaving a frozen slice's rows untouched changes
+// nothing on the active ones.  active == nullptr: no skipping.
+struct SliceSkip {
+  const double* active;   // [nslices] 1.0 / 0.0
+  const int* slice_of;    // row -> slice (coarse levels), or nullptr: slice = row / L
+  long long L;
+  __device__ __forceinline__ bool skip(long long r) const {
+    if (!active) return false;
+    long long k = slice_of ? (long long)slice_of[r] : r / L;
+    return active[k] == 0.0;
+  }
+};
+
 struct AmgLevel {
   long long n = 0, nc = 0;
   // CSR (levels >= 1)
@@ -117,6 +131,7 @@ struct AmgLevel {
   DBuf<long long> mptr;   // coarse row -> members (ascending)
   DBuf<int> midx;
   DBuf<double> b, x, r, xt;      // x: pre-smoothed iterate; xt: this level's V-cycle output
+  DBuf<double> kc1, kv, krc;     // K-cycle work vectors (mode A tail levels)
   std::vector<long long> sptr;   // host slice pointers
   DBuf<long long> dsptr;         // the same on the device (per-slice coarse tail)
   DBuf<long long> sl_off;        // SELL-32 copy of the CSR (V-cycle sweeps)
@@ -136,6 +151,7 @@ struct AmgHierarchy {
   int cm = 0;              // mode A: max rows per slice - 1; mode T: nc
   DBuf<long long> csptr;   // mode A: coarsest slice pointers (device)
   int tail = 0;            // mode A: first level handled by the per-slice tail kernel
+  DBuf<char> tail_args;    // mode A: the tail kernel's level table (device, TailArgs)
   bool ready = false;
   void clear() { lv.clear(); ready = false; }
 };
@@ -154,6 +170,6 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
 // runs fuse->fin (the PCG r.z step); returns true iff it did.
 template <class V0>
 bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x,
-                const SliceDotFuse* fuse = nullptr);
+                const SliceDotFuse* fuse = nullptr, const double* active = nullptr);
 
 }  // namespace bbot

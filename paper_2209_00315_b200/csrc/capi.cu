@@ -101,6 +101,10 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
       BB_CUDA(cudaDeviceGetDefaultMemPool(&pool, devid));
       unsigned long long thr = ~0ULL;
       BB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      // the AMG(A) tail kernel recurses through the K-cycle levels (depth <= 2 x levels)
+      size_t stk = 0;
+      BB_CUDA(cudaDeviceGetLimit(&stk, cudaLimitStackSize));
+      if (stk < 4096) BB_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 4096));
     }
     BB_CUDA(cudaDeviceGetAttribute(&c->dev.num_sms, cudaDevAttrMultiProcessorCount, devid));
     c->red.init(&c->dev, std::max(K + 2, 64));

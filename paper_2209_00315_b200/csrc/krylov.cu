@@ -309,6 +309,7 @@ __global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double
   long long beg, end;
   red_chunk(L, R.parts, beg, end);
   double acc = 0.0;
+  if (fin.s[PS_ACTIVE * gridDim.y + k] == 0.0) end = beg;   // converged slice
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) acc += r[(size_t)k * L + i] * z[(size_t)k * L + i];
   if (red_commit(acc, R)) fin(R.out);
 }
@@ -321,6 +322,7 @@ __global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict
   const double a = s[PS_ALPHA * ns + k];
   long long beg, end;
   red_chunk(L, R.parts, beg, end);
+  if (s[PS_ACTIVE * ns + k] == 0.0) end = beg;   // converged slice: frozen
   double acc = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     size_t t = (size_t)k * L + i;

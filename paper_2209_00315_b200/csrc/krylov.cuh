@@ -96,6 +96,7 @@ __global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double*
   double beta = s[PS_BETA * ns + k];
   long long beg, end;
   red_chunk(L, R.parts, beg, end);
+  if (s[PS_ACTIVE * ns + k] == 0.0) end = beg;   // converged slice: frozen, nothing to do
   double acc = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     long long row = (long long)k * L + i;
@@ -124,7 +125,7 @@ void DevPcg::emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const dou
   launch(d, k_pcg_start, dim3(parts, ns), dim3(BS), 0, L, b, r.p, S, its.p, sc.p, maxit,
          red.args(parts, ns, out));
   dev_while(d, dev_field(sc.p, &PcgScal::flag), [&](const LoopCtl& ctl) {
-    SliceDotFuse fz{red.args(parts, ns, out), parts, ns, L, PcgRzFin{S, sc.p, ns}};
+    SliceDotFuse fz{red.args(parts, ns, out), parts, ns, L, PcgRzFin{S, sc.p, ns}, S + PS_ACTIVE * ns};
     if (!pre(r.p, z.p, &fz))
       launch(d, k_pcg_rz, dim3(parts, ns), dim3(BS), 0, L, (const double*)r.p, (const double*)z.p, fz.R, fz.fin);
     launch(d, k_pcg_pq<V>, dim3(parts, ns), dim3(BS), 0, view, L, (const double*)z.p, p.p, q.p, (const double*)S,

@@ -63,6 +63,7 @@ struct SliceDotFuse {
   int parts, ns;
   long long L;
   PcgRzFin fin;
+  const double* active;   // [ns] slices still iterating (others are skipped by the producer)
 };
 
 }  // namespace bbot

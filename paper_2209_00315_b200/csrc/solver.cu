@@ -99,7 +99,9 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   LapView vA = view_A(c);
   c->pcg.emit(
       c->dev, c->red, vA,
-      [&](const double* x, double* y, const SliceDotFuse* f) { return amg_vcycle(c->dev, c->amgA, vA, x, y, f); },
+      [&](const double* x, double* y, const SliceDotFuse* f) {
+        return amg_vcycle(c->dev, c->amgA, vA, x, y, f, f ? f->active : nullptr);
+      },
       c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner);
   remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
 }

@@ -320,3 +320,26 @@ def test_direction_parity_C2_bench_system():
     assert abs(st["outer_its"] - S.stats["outer_its"]) <= 1, (st, S.stats)
     for a, b in ((dphi, ophi), (drho, orho), (ds, os_)):
         assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_amg_kcycle_parity():
+    """The K-cycle coarse corrections of AMG(A) (I3: hierarchies of >= 7 levels, levels
+    with <= 4096 rows per slice) -- exercised on C2 with the coarsest block cut to 2
+    rows per slice (7 levels): identical aggregates, V-cycle output to 1e-10."""
+    pb = _gpu()
+    p = make_problem("C2")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=3, mu=1e-2)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, opts=pb.default_solver_opts(coarse_max_A=2))
+    ctx.set_state(phi, rho, s, 1e-2)
+    ctx.assemble()
+    slA = np.repeat(np.arange(d.K + 1), d.N)
+    H = oamg.setup(d.A(rho), slA, "A", 2.0 / 3.0, 2)
+    assert len(H.levels) >= oamg.KC_MIN_LEVELS and any(H.kcycle)
+    sizes = ctx.amg_info(0)
+    assert sizes == H.sizes
+    for lvl in range(len(sizes) - 1):
+        assert np.array_equal(ctx.amg_agg(0, lvl), H.levels[lvl].agg), lvl
+    b = np.random.default_rng(5).standard_normal(sizes[0]).reshape(d.K + 1, d.N)
+    b = (b - b.mean(1, keepdims=True)).reshape(-1)
+    assert _rel(ctx.amg_vcycle(0, b), oamg.vcycle(H, b)) < 1e-10
