@@ -104,22 +104,28 @@ class ClockSampler:
 
 def byte_models(ctx, nnzT):
     """Algorithmic (compulsory) bytes per launch of the main kernels.
-    fp64 = 8 B, int32 = 4 B; geometry tables shared by all time slices count once."""
-    n, m, N, NE, K, nbar = ctx.n, ctx.m, ctx.N, ctx.NE, ctx.K, ctx.nbar
+    fp64 = 8 B, int32 = 4 B; geometry tables shared by all time slices count once.
+    A_k is read in cell-ELL form (Aoff [K+1][4][N] = 32 B per row, neighbour table
+    [4][N] int32 once); T level 0 as slice-shared ELL (values 8 B per stored entry,
+    column pattern [W][nbar] int32 once)."""
+    n, m, N, K, nbar = ctx.n, ctx.m, ctx.N, ctx.K, ctx.nbar
     W = ctx.T_width
     A_sizes, T_sizes = ctx.amg_info(0), ctx.amg_info(1)
     nc1A = A_sizes[1] if len(A_sizes) > 1 else 0
     nc1T = T_sizes[1] if len(T_sizes) > 1 else 0
-    om = 8 * (K + 1) * NE + 32 * N          # edge weights omega + cell->edge tables [4][N] x2 (once)
+    lapA = 32 * n + 16 * N                  # Aoff + neighbour table
     tT = 8 * nnzT + 4 * W * nbar            # T values + shared column pattern
     return {
-        # per-slice PCG (I4): p = z + beta p, q = A z + beta q, p.q   (reads z p q, writes p q)
-        "void bbot::k_pcg_pq<bbot::LapView>": 40 * n + om,
-        "bbot::k_pcg_xr": 48 * n,                      # x += a p, r -= a q, r.r
+        # per-slice PCG (I4): p = z + beta p, q = A z + beta q, p.q  (read z p q, write p q)
+        "void bbot::k_pcg_pq<bbot::LapView>": 40 * n + lapA,
+        "bbot::k_pcg_xr": 48 * n,                      # x += a p, r -= a q, r.r  (read x r p q, write x r)
         "bbot::k_pcg_rz": 16 * n,
-        "void bbot::k_spmv<bbot::LapView>": 16 * n + om,
-        "void bbot::k_down<bbot::LapView>": 32 * n + om,
-        "void bbot::k_up<bbot::LapView>": 36 * n + 8 * nc1A + om,
+        # level-0 V-cycle sweeps of AMG(A): k_down reads b dinv, writes x r; k_up_dot reads b x
+        # dinv agg(4 B) and the level-1 correction, writes z (r.z fused)
+        "void bbot::k_down<bbot::LapView>": 32 * n + lapA,
+        "void bbot::k_up_dot<bbot::LapView>": 36 * n + 8 * nc1A + lapA,
+        "void bbot::k_up<bbot::LapView>": 36 * n + 8 * nc1A + lapA,
+        "void bbot::k_spmv<bbot::LapView>": 16 * n + lapA,
         "void bbot::k_spmv<bbot::SliceEllView>": tT + 16 * m,
         "void bbot::k_down<bbot::SliceEllView>": tT + 32 * m,
         "void bbot::k_up<bbot::SliceEllView>": tT + 36 * m + 8 * nc1T,
@@ -339,7 +345,7 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: first IPM Newton system (A19 point, mu=1), eps_out=1e-10",
-                       "nbar": ctx.nbar, "K": ctx.K, "n_plus_m": ctx.n + ctx.m,
+                       "nbar": ctx.nbar, "K": ctx.K, "n_plus_m": ctx.n + ctx.m, "T_width": ctx.T_width,
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "no flush; per-step working set (FGMRES basis 61 x (n+m) x 8 B) exceeds the 126 MB L2"},
             "unknowns_per_s": value * (ctx.n + ctx.m),

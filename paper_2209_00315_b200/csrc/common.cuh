@@ -293,18 +293,18 @@ struct Reducer {
   void init(Dev* d, int max_slices) {
     dev = d;
     // (parts <= 1024) x (<= 33 CGS2 dots) covers every multi-result reduction
-    cap = std::max((size_t)16 * d->num_sms + 2 * (size_t)max_slices + 4096, (size_t)1024 * 33);
+    cap = std::max((size_t)64 * d->num_sms + 2 * (size_t)max_slices + 4096, (size_t)4096 * 33);
     partial.alloc(cap, d->stream);
     counter.alloc(1, d->stream);
     counter.zero();
   }
-  // blocks per slice: ~512 elements per block (2 per thread: enough loads in
-  // flight), <= 16 blocks per SM in total
+  // blocks per slice: ~512 elements per block (2 per thread), <= 64 blocks per
+  // SM in total (several waves: enough independent loads in flight for HBM)
   int parts_for(long long len, int nslices) const {
     long long p = (len + 511) / 512;
-    long long cap_b = std::max(1LL, (long long)(16 * dev->num_sms) / std::max(1, nslices));
+    long long cap_b = std::max(1LL, (long long)(64 * dev->num_sms) / std::max(1, nslices));
     p = std::min(p, cap_b);
-    p = std::min(p, 1024LL);
+    p = std::min(p, 4096LL);
     return (int)std::max(1LL, p);
   }
   RedArgs args(int parts, int nslices, double* out) {
