@@ -405,15 +405,19 @@ __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, cons
 // ------------------------------------------------------------ per-slice coarse tail (mode A)
 // AMG(A) never aggregates across time slices (I3), so below the first level with
 // <= TAIL_ROWS rows per slice the rest of the cycle is independent per slice:
-// one CTA per slice runs the restriction from level tail-1 and the whole coarse
-// cycle -- damped-Jacobi V(1,1) steps, the K-cycle coarse corrections (two
-// flexible-CG steps with per-slice block reductions, I3/oracle kstep) and the
-// grounded coarsest solve -- separated by __syncthreads() instead of launches.
-// The level table lives in device memory (TailArgs), read through a pointer.
-constexpr int TAIL_ROWS = 4096;      // == oracle KC_ROWS: the tail levels are the K-cycle candidates
+// one thread-block CLUSTER per slice (CL CTAs, CL = 148 / slices, <= 8) runs the
+// restriction from level tail-1 and the whole coarse cycle -- damped-Jacobi
+// V(1,1) steps, the K-cycle coarse corrections (two flexible-CG steps, per-slice
+// dots reduced across the cluster through distributed shared memory in a fixed
+// order; I3 / oracle amg.kstep) and the grounded coarsest solve -- with cluster
+// barriers (barrier.cluster, release/acquire) instead of kernel launches.  The
+// level table lives in device memory (TailArgs), read through a pointer.
+constexpr int TAIL_ROWS = 8192;      // first tail level: <= TAIL_ROWS rows per slice (GPU-only choice)
+constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
 constexpr int TAIL_MAXL = 24;
 constexpr int TAIL_BS = 1024;
+constexpr int TAIL_MAXCL = 8;
 
 struct TailLevel {
   SellView A;
@@ -438,62 +442,72 @@ struct TailArgs {
   TailLevel lv[TAIL_MAXL];
 };
 
-// per-slice dot over rows [s0, s1): block reduction, result broadcast to all threads
-__device__ __forceinline__ double tail_dot(const double* u, const double* v, long long s0, long long s1) {
-  __shared__ double res;
+struct TailPos {               // this CTA: slice k, rank c of cs CTAs in the slice's cluster
+  int k, c, cs;
+  __device__ long long first_row(long long s0) const { return s0 + (long long)c * blockDim.x + threadIdx.x; }
+  __device__ long long stride() const { return (long long)cs * blockDim.x; }
+};
+
+__device__ __forceinline__ void tail_sync() { cg::this_cluster().sync(); }
+
+// per-slice dot over rows [s0, s1): block sums, then every CTA adds the cluster's
+// partials in rank order (identical result everywhere)
+__device__ __forceinline__ double tail_dot(const double* u, const double* v, long long s0, long long s1,
+                                           const TailPos& P) {
+  __shared__ double part;
   double acc = 0.0;
-  for (long long r = s0 + threadIdx.x; r < s1; r += blockDim.x) acc += u[r] * v[r];
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) acc += u[r] * v[r];
   acc = block_sum(acc);
-  if (threadIdx.x == 0) res = acc;
-  __syncthreads();
-  double out = res;
-  __syncthreads();
-  return out;
+  if (threadIdx.x == 0) part = acc;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  double tot = 0.0;
+  for (int q = 0; q < P.cs; q++) tot += *cl.map_shared_rank(&part, q);
+  cl.sync();
+  return tot;
 }
 __device__ __forceinline__ double tail_div(double a, double b) { return b != 0.0 ? a / b : 0.0; }
 
-__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k);
+__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos& P);
 
 // K-cycle step at tail level q: input lv[q].b (= rc), output lv[q].xo (oracle amg.kstep)
-__device__ void tail_kstep(const TailArgs* __restrict__ T, int q, int k) {
+__device__ void tail_kstep(const TailArgs* __restrict__ T, int q, const TailPos& P) {
   const TailLevel& L = T->lv[q];
-  const long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
-  const int tid = threadIdx.x, bs = blockDim.x;
-  for (long long r = s0 + tid; r < s1; r += bs) L.krc[r] = L.b[r];
-  __syncthreads();
-  tail_cycle(T, q, k);                                   // c1 -> xo
-  for (long long r = s0 + tid; r < s1; r += bs) {
-    double c = L.xo[r];
-    L.kc1[r] = c;
+  const long long s0 = L.sptr[P.k], s1 = L.sptr[P.k + 1];
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.krc[r] = L.b[r];
+  tail_sync();
+  tail_cycle(T, q, P);                                   // c1 -> xo
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
+    L.kc1[r] = L.xo[r];
     double av = 0.0;
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
     L.kv[r] = av;                                        // v1 = A c1
   }
-  __syncthreads();
-  const double rho1 = tail_dot(L.kc1, L.kv, s0, s1);
-  const double a1 = tail_dot(L.kc1, L.krc, s0, s1);
+  tail_sync();
+  const double rho1 = tail_dot(L.kc1, L.kv, s0, s1, P);
+  const double a1 = tail_dot(L.kc1, L.krc, s0, s1, P);
   const double f1 = tail_div(a1, rho1);
-  for (long long r = s0 + tid; r < s1; r += bs) L.b[r] = L.krc[r] - f1 * L.kv[r];   // r2
-  __syncthreads();
-  tail_cycle(T, q, k);                                   // c2 -> xo
-  const double g = tail_dot(L.xo, L.kv, s0, s1);
-  const double a2 = tail_dot(L.xo, L.b, s0, s1);
-  for (long long r = s0 + tid; r < s1; r += bs) {
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.b[r] = L.krc[r] - f1 * L.kv[r];   // r2
+  tail_sync();
+  tail_cycle(T, q, P);                                   // c2 -> xo
+  const double g = tail_dot(L.xo, L.kv, s0, s1, P);
+  const double a2 = tail_dot(L.xo, L.b, s0, s1, P);
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
     double av = 0.0;
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
     L.kv[r] = av;                                        // v2 = A c2
   }
-  __syncthreads();
-  const double beta = tail_dot(L.xo, L.kv, s0, s1);
+  tail_sync();
+  const double beta = tail_dot(L.xo, L.kv, s0, s1, P);
   const double rho2 = beta - g * tail_div(g, rho1);
   const double g2 = tail_div(a2, rho2);
   const double e1 = f1 - g * tail_div(g2, rho1);
-  for (long long r = s0 + tid; r < s1; r += bs) L.xo[r] = e1 * L.kc1[r] + g2 * L.xo[r];
-  __syncthreads();
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.xo[r] = e1 * L.kc1[r] + g2 * L.xo[r];
+  tail_sync();
 }
 
 // cycle of tail level q: input lv[q].b, output lv[q].xo
-__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k) {
+__device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos& P) {
   const int tid = threadIdx.x, bs = blockDim.x;
   const int nl = T->last - T->first;
   const double om = T->om;
@@ -501,10 +515,10 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k) {
     __shared__ double xs[128];
     __shared__ double mean;
     const TailLevel& C = T->lv[nl];
-    long long s0 = C.sptr[k];
-    int nloc = (int)(C.sptr[k + 1] - s0);
-    const double* inv = T->cinv + (size_t)k * T->cm * T->cm;
-    for (int j = tid; j < nloc; j += bs) {
+    long long s0 = C.sptr[P.k];
+    int nloc = (int)(C.sptr[P.k + 1] - s0);
+    const double* inv = T->cinv + (size_t)P.k * T->cm * T->cm;
+    for (int j = tid; j < nloc; j += bs) {      // every CTA of the cluster computes it (tiny)
       double acc = 0.0;
       if (j > 0)
         for (int l = 1; l < nloc; l++) acc += inv[(j - 1) * T->cm + (l - 1)] * C.b[s0 + l];
@@ -518,54 +532,142 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, int k) {
       if (tid == 0) mean = nloc > 0 ? sum / nloc : 0.0;
     }
     __syncthreads();
-    for (int j = tid; j < nloc; j += bs) C.xo[s0 + j] = xs[j] - mean;
-    __syncthreads();
+    if (P.c == 0)
+      for (int j = tid; j < nloc; j += bs) C.xo[s0 + j] = xs[j] - mean;
+    tail_sync();
     return;
   }
   const TailLevel& L = T->lv[q];
-  const long long s0 = L.sptr[k], s1 = L.sptr[k + 1];
-  for (long long r = s0 + tid; r < s1; r += bs) {
+  const long long s0 = L.sptr[P.k], s1 = L.sptr[P.k + 1];
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
     double acc = L.b[r];
     L.A.row(r, [&](long long c, double a) { acc -= a * (om * L.dinv[c] * L.b[c]); });
     L.x[r] = om * L.dinv[r] * L.b[r];
     L.r[r] = acc;
   }
-  __syncthreads();
+  tail_sync();
   const TailLevel& C = T->lv[q + 1];
-  const long long c0 = C.sptr[k], c1 = C.sptr[k + 1];
-  for (long long I = c0 + tid; I < c1; I += bs) {
+  const long long c0 = C.sptr[P.k], c1 = C.sptr[P.k + 1];
+  for (long long I = P.first_row(c0); I < c1; I += P.stride()) {
     double acc = 0.0;
     for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
     C.b[I] = acc;
   }
-  __syncthreads();
-  if (C.kc) tail_kstep(T, q + 1, k);
-  else tail_cycle(T, q + 1, k);
+  tail_sync();
+  if (C.kc) tail_kstep(T, q + 1, P);
+  else tail_cycle(T, q + 1, P);
   const double* xc = C.xo;
-  for (long long r = s0 + tid; r < s1; r += bs) {
+  for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
     double acc = L.b[r];
     L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
     L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
   }
-  __syncthreads();
+  tail_sync();
 }
 
 __global__ void __launch_bounds__(TAIL_BS) k_tailA(const TailArgs* __restrict__ T, const double* active) {
-  const int k = blockIdx.x;
-  if (active && active[k] == 0.0) return;        // converged slice
-  const int tid = threadIdx.x, bs = blockDim.x;
+  cg::cluster_group cl = cg::this_cluster();
+  TailPos P{(int)(blockIdx.x / cl.num_blocks()), (int)cl.block_rank(), (int)cl.num_blocks()};
+  if (active && active[P.k] == 0.0) return;        // converged slice (the whole cluster leaves)
   {   // restriction from level first-1 (rows of slice k at level `first` are contiguous)
     const TailLevel& F = T->lv[0];
-    long long s0 = F.sptr[k], s1 = F.sptr[k + 1];
-    for (long long I = s0 + tid; I < s1; I += bs) {
+    long long s0 = F.sptr[P.k], s1 = F.sptr[P.k + 1];
+    for (long long I = P.first_row(s0); I < s1; I += P.stride()) {
       double acc = 0.0;
       for (long long p = T->mptr0[I]; p < T->mptr0[I + 1]; p++) acc += T->r0[T->midx0[p]];
       F.b[I] = acc;
     }
   }
-  __syncthreads();
-  if (T->lv[0].kc) tail_kstep(T, 0, k);
-  else tail_cycle(T, 0, k);
+  tail_sync();
+  if (T->lv[0].kc) tail_kstep(T, 0, P);
+  else tail_cycle(T, 0, P);
+}
+
+// ------------------------------------------------------------ coarse tail of AMG(T)
+// T couples neighbouring time slices, so its coarse levels are not independent per
+// slice; instead ONE cluster of up to 16 CTAs (16 K threads, one row each at the
+// first tail level) runs every level with <= TAILT_ROWS rows -- pre-smoothing +
+// residual + restriction, the dense coarsest solve (warp per row), prolongation +
+// post-smoothing -- separated by cluster barriers: a dozen latency-bound launches
+// per V-cycle become one.  Arithmetic per row is that of k_down/k_restrict/
+// k_dense_mv/k_up (same order).
+constexpr int TAILT_ROWS = 16384;
+
+struct TailTLevel {
+  SellView A;
+  long long n;
+  const double* dinv;
+  double *b, *x, *r, *xo;
+  const long long* mptr;
+  const int* midx;
+  const int* agg;
+};
+struct TailTArgs {
+  int first, last;
+  double om;
+  int nc;                       // coarsest size (dense inverse nc x nc)
+  const double* cinv;
+  const long long* mptr0;
+  const int* midx0;
+  const double* r0;
+  TailTLevel lv[TAIL_MAXL];
+};
+
+__global__ void __launch_bounds__(TAIL_BS) k_tailT(const TailTArgs* __restrict__ T) {
+  cg::cluster_group cl = cg::this_cluster();
+  const long long g0 = (long long)cl.block_rank() * blockDim.x + threadIdx.x;
+  const long long gs = (long long)cl.num_blocks() * blockDim.x;
+  const double om = T->om;
+  const int nl = T->last - T->first;
+  {
+    const TailTLevel& F = T->lv[0];
+    for (long long I = g0; I < F.n; I += gs) {
+      double acc = 0.0;
+      for (long long p = T->mptr0[I]; p < T->mptr0[I + 1]; p++) acc += T->r0[T->midx0[p]];
+      F.b[I] = acc;
+    }
+  }
+  cl.sync();
+  for (int q = 0; q < nl; q++) {
+    const TailTLevel& L = T->lv[q];
+    for (long long r = g0; r < L.n; r += gs) {
+      double acc = L.b[r];
+      L.A.row(r, [&](long long c, double a) { acc -= a * (om * L.dinv[c] * L.b[c]); });
+      L.x[r] = om * L.dinv[r] * L.b[r];
+      L.r[r] = acc;
+    }
+    cl.sync();
+    const TailTLevel& C = T->lv[q + 1];
+    for (long long I = g0; I < C.n; I += gs) {
+      double acc = 0.0;
+      for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
+      C.b[I] = acc;
+    }
+    cl.sync();
+  }
+  {   // coarsest: x = inv(T_c) b, one warp per row (as k_dense_mv)
+    const TailTLevel& C = T->lv[nl];
+    const int n = T->nc;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = g0 >> 5, ws = gs >> 5;
+    for (long long row = w0; row < n; row += ws) {
+      double acc = 0.0;
+      for (int j = lane; j < n; j += 32) acc += T->cinv[(size_t)row * n + j] * C.b[j];
+      acc = warp_sum(acc);
+      if (lane == 0) C.xo[row] = acc;
+    }
+  }
+  cl.sync();
+  for (int q = nl - 1; q >= 0; q--) {
+    const TailTLevel& L = T->lv[q];
+    const double* xc = T->lv[q + 1].xo;
+    for (long long r = g0; r < L.n; r += gs) {
+      double acc = L.b[r];
+      L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
+      L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
+    }
+    cl.sync();
+  }
 }
 
 // mode T: dense Gauss-Jordan in global memory, two launches per pivot
@@ -833,6 +935,7 @@ std::vector<long long> slice_ptrs(Dev& d, const int* sl, long long n, int nslice
 }  // namespace
 
 static void tail_args(AmgHierarchy& H, TailArgs& T);
+static double* level_out(AmgHierarchy& H, int l);
 
 template <class V0>
 void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nslices, int mode, double omega,
@@ -958,8 +1061,50 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     sync(d);
   }
   for (size_t l = 1; l < H.lv.size(); l++) build_sell(d, H.lv[l], w);
+  // mode T: the coarse tail starts at the first coarse level with <= TAILT_ROWS rows
+  if (mode == 1 && H.lv.size() >= 3) {
+    int L = (int)H.lv.size();
+    H.tail = 0;
+    for (int l = 1; l < L - 1; l++)
+      if (H.lv[l].n <= TAILT_ROWS && L - l <= TAIL_MAXL) { H.tail = l; break; }
+    if (H.tail > 0) {
+      static TailTArgs hostTT;
+      AmgLevel& P = H.lv[H.tail - 1];
+      hostTT.first = H.tail;
+      hostTT.last = L - 1;
+      hostTT.om = H.omega;
+      hostTT.nc = (int)H.lv[L - 1].n;
+      hostTT.cinv = H.cinv.p;
+      hostTT.mptr0 = P.mptr.p;
+      hostTT.midx0 = P.midx.p;
+      hostTT.r0 = P.r.p;
+      for (int l = H.tail; l < L; l++) {
+        AmgLevel& A = H.lv[l];
+        TailTLevel& t = hostTT.lv[l - H.tail];
+        t.A = A.sell();
+        t.n = A.n;
+        t.dinv = A.dinv.p;
+        t.b = A.b.p;
+        t.x = A.x.p;
+        t.r = A.r.p;
+        t.xo = level_out(H, l);
+        t.mptr = A.mptr.p;
+        t.midx = A.midx.p;
+        t.agg = A.agg.p;
+      }
+      H.tail_args.alloc(sizeof(TailTArgs), s);
+      BB_CUDA(cudaMemcpyAsync(H.tail_args.p, &hostTT, sizeof(TailTArgs), cudaMemcpyHostToDevice, s));
+      H.tail_cl = 16;
+      static bool attr_done = false;
+      if (!attr_done) {
+        BB_CUDA(cudaFuncSetAttribute(k_tailT, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_done = true;
+      }
+      sync(d);
+    }
+  }
   // mode A: the per-slice tail starts at the first coarse level with <= TAIL_ROWS rows per slice
-  H.tail = 0;
+  if (mode == 0) H.tail = 0;
   if (mode == 0 && H.lv.size() >= 2) {
     int L = (int)H.lv.size();
     for (int l = 1; l < L; l++) {
@@ -1032,7 +1177,9 @@ static void tail_args(AmgHierarchy& H, TailArgs& T) {
     t.midx = A.midx.p;
     t.agg = A.agg.p;
     t.sptr = A.dsptr.p;
-    t.kc = (L >= KC_MIN_LEVELS && l < L - 1) ? 1 : 0;   // K-cycle levels (oracle amg.setup kcycle)
+    long long mx = 0;
+    for (int k = 0; k < H.nslices; k++) mx = std::max(mx, A.sptr[k + 1] - A.sptr[k]);
+    t.kc = (L >= KC_MIN_LEVELS && l < L - 1 && mx <= KC_ROWS) ? 1 : 0;   // K-cycle levels (oracle amg.setup)
   }
 }
 
@@ -1046,7 +1193,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
   const long long L0 = H.lv[0].n / std::max(1, H.nslices);
   auto skip_at = [&](int l) { return SliceSkip{active, l == 0 ? nullptr : (const int*)H.lv[l].slice_of.p, L0}; };
   // grid-wide levels: 0 .. stop-1; below: the per-slice tail (mode A) or more grid levels
-  int stop = (H.mode == 0 && H.tail > 0) ? H.tail : L - 1;
+  int stop = H.tail > 0 ? H.tail : L - 1;
   for (int l = 0; l < stop; l++) {
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
@@ -1055,12 +1202,15 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     else
       launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, lv.x.p, lv.r.p, skip_at(l));
-    if (!(H.mode == 0 && H.tail > 0 && l == stop - 1))
+    if (!(H.tail > 0 && l == stop - 1))
       launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
              (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1));
   }
   if (H.mode == 0 && H.tail > 0) {
-    launch(d, k_tailA, dim3(H.nslices), dim3(TAIL_BS), 0, (const TailArgs*)H.tail_args.p, active);
+    int cl = std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
+    launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(TAIL_BS), 0, cl, (const TailArgs*)H.tail_args.p, active);
+  } else if (H.tail > 0) {
+    launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p);
   } else {
     coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
   }

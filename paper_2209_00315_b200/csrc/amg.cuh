@@ -151,9 +151,10 @@ struct AmgHierarchy {
   int cm = 0;              // mode A: max rows per slice - 1; mode T: nc
   DBuf<long long> csptr;   // mode A: coarsest slice pointers (device)
   int tail = 0;            // mode A: first level handled by the per-slice tail kernel
-  DBuf<char> tail_args;    // mode A: the tail kernel's level table (device, TailArgs)
+  DBuf<char> tail_args;    // the tail kernel's level table (device; TailArgs / TailTArgs)
+  int tail_cl = 1;         // cluster size of the tail launch
   bool ready = false;
-  void clear() { lv.clear(); ready = false; }
+  void clear() { lv.clear(); ready = false; tail = 0; tail_cl = 1; }
 };
 
 struct AmgWork {

@@ -93,6 +93,40 @@ inline void launch(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, Args...
   }
 }
 
+// launch with a thread-block cluster of `cl` CTAs along x (grid.x multiple of cl)
+template <class K, class... Args>
+inline void launch_cluster(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, int cl, Args... args) {
+  if (grid.x == 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = d.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ProfRec r{(const void*)kernel, nullptr, nullptr};
+  bool prof = d.prof && !d.capturing;
+  if (prof) {
+    r.a = d.get_event();
+    r.b = d.get_event();
+    cudaEventRecord(r.a, d.stream);
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (prof) {
+    cudaEventRecord(r.b, d.stream);
+    d.recs.push_back(r);
+  }
+  if (!d.capturing) d.launches++;
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess && d.sync_check && !d.capturing) e = cudaStreamSynchronize(d.stream);
+  if (e != cudaSuccess) throw Error(BBOT_E_CUDA, std::string("cluster kernel launch: ") + cudaGetErrorString(e));
+}
+
 inline unsigned nblocks(long long n, int bs, long long cap = 1LL << 30) {
   long long b = (n + bs - 1) / bs;
   if (b < 1) b = 1;

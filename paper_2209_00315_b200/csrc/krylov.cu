@@ -109,25 +109,25 @@ __global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __
 
 // h[k] = V[k] . w for k <= j (one pass over w, one register accumulator per k);
 // optionally copy zout -> Z[j] in the same pass
-template <bool COPYZ>
+template <bool COPYZ, int NR>
 __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __restrict__ V,
                                                  const double* __restrict__ w, const double* __restrict__ zout,
                                                  double* __restrict__ Z, GmresScal* G, int which, RedArgs R) {
   const int j = G->j;
   long long beg, end;
   red_chunk(n, R.parts, beg, end);
-  double acc[GM_MAXR];
+  double acc[NR];
 #pragma unroll
-  for (int k = 0; k < GM_MAXR; k++) acc[k] = 0.0;
+  for (int k = 0; k < NR; k++) acc[k] = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double wi = w[i];
     if (COPYZ) Z[(size_t)j * n + i] = zout[i];
 #pragma unroll
-    for (int k = 0; k < GM_MAXR; k++)
+    for (int k = 0; k < NR; k++)
       if (k <= j) acc[k] += V[(size_t)k * n + i] * wi;
   }
 #pragma unroll
-  for (int k = 0; k < GM_MAXR; k++) {
+  for (int k = 0; k < NR; k++) {
     if (k <= j) {
       double s = block_sum(acc[k]);
       if (threadIdx.x == 0) R.partial[(size_t)k * R.parts + blockIdx.x] = s;
@@ -136,6 +136,48 @@ __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __re
   if (!red_last_block(R.counter)) return;
   double* out = which == 0 ? G->h1 : G->h2;
   red_finish(R.partial, R.parts, j + 1, out);
+}
+
+// CGS2 middle step in one pass: w -= sum_{k<=j} h1[k] V[k] (first projection),
+// then h2[k] = V[k] . w for the second, reusing the V entries just loaded
+template <int NR>
+__global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double* __restrict__ V,
+                                                      double* __restrict__ w, GmresScal* G, RedArgs R) {
+  const int j = G->j;
+  __shared__ double hs[GM_MAXR + 1];
+  if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = G->h1[threadIdx.x];
+  __syncthreads();
+  long long beg, end;
+  red_chunk(n, R.parts, beg, end);
+  double acc[NR];
+#pragma unroll
+  for (int k = 0; k < NR; k++) acc[k] = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double vk[NR];
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NR; k++) {
+      vk[k] = 0.0;
+      if (k <= j) {
+        vk[k] = V[(size_t)k * n + i];
+        s += hs[k] * vk[k];
+      }
+    }
+    double v = w[i] - s;
+    w[i] = v;
+#pragma unroll
+    for (int k = 0; k < NR; k++)
+      if (k <= j) acc[k] += vk[k] * v;
+  }
+#pragma unroll
+  for (int k = 0; k < NR; k++) {
+    if (k <= j) {
+      double t = block_sum(acc[k]);
+      if (threadIdx.x == 0) R.partial[(size_t)k * R.parts + blockIdx.x] = t;
+    }
+  }
+  if (!red_last_block(R.counter)) return;
+  red_finish(R.partial, R.parts, j + 1, G->h2);
 }
 
 // w -= sum_{k<=j} h[k] V[k]  (h = h1 or h2); with GIVENS: partial ||w||^2 and,
@@ -255,12 +297,18 @@ void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, con
       pre(vin.p, zout.p);
       op(zout.p, w.p);
       // CGS2: two classical Gram-Schmidt passes
-      launch(d, k_gm_dots<true>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
-             (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
-      launch(d, k_gm_orth<false>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G, 0,
-             red.args(parts, 1, nullptr), inner);
-      launch(d, k_gm_dots<false>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
-             (const double*)nullptr, (double*)nullptr, G, 1, red.args(parts, restart + 1, nullptr));
+      if (restart <= 12)
+        launch(d, k_gm_dots<true, 12>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+               (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
+      else
+        launch(d, k_gm_dots<true, GM_MAXR>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+               (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
+      if (restart <= 12)
+        launch(d, k_gm_orth_dots<12>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G,
+               red.args(parts, restart + 1, nullptr));
+      else
+        launch(d, k_gm_orth_dots<GM_MAXR>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G,
+               red.args(parts, restart + 1, nullptr));
       launch(d, k_gm_orth<true>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G, 1,
              red.args(parts, 1, rout), inner);
       launch(d, k_gm_scale, dim3(nb), dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0);
