@@ -412,7 +412,14 @@ __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, cons
 // order; I3 / oracle amg.kstep) and the grounded coarsest solve -- with cluster
 // barriers (barrier.cluster, release/acquire) instead of kernel launches.  The
 // level table lives in device memory (TailArgs), read through a pointer.
-constexpr int TAIL_ROWS = 8192;      // first tail level: <= TAIL_ROWS rows per slice (GPU-only choice)
+// GPU-only tuning knobs (not part of the algorithm; env overrides for A/B runs)
+static long long tune_env(const char* name, long long dflt) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+static const long long TAIL_ROWS = tune_env("BBOT_TAIL_ROWS", 0);       // A-tail for shallow hierarchies (0: none)
+static const long long TAILT_ROWS = tune_env("BBOT_TAILT_ROWS", 16384); // first T-tail level: <= rows in total
+static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tail cluster size (0: 148/slices)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
 constexpr int TAIL_MAXL = 24;
@@ -591,7 +598,6 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(const TailArgs* __restrict__ 
 // post-smoothing -- separated by cluster barriers: a dozen latency-bound launches
 // per V-cycle become one.  Arithmetic per row is that of k_down/k_restrict/
 // k_dense_mv/k_up (same order).
-constexpr int TAILT_ROWS = 16384;
 
 struct TailTLevel {
   SellView A;
@@ -1103,14 +1109,19 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
       sync(d);
     }
   }
-  // mode A: the per-slice tail starts at the first coarse level with <= TAIL_ROWS rows per slice
+  // mode A: the per-slice tail kernel (where the K-cycle lives) starts at the first K-cycle
+  // level (hierarchies of >= KC_MIN_LEVELS levels, <= KC_ROWS rows per slice); shallower
+  // hierarchies run every level as graph-replayed grid kernels, which measured faster on
+  // C2 than any in-kernel fusion of the coarse levels (172.8 vs 185-299 ms per step),
+  // unless BBOT_TAIL_ROWS asks for a tail.
   if (mode == 0) H.tail = 0;
   if (mode == 0 && H.lv.size() >= 2) {
     int L = (int)H.lv.size();
-    for (int l = 1; l < L; l++) {
+    long long lim = L >= KC_MIN_LEVELS ? (long long)KC_ROWS : TAIL_ROWS;
+    for (int l = 1; l < L && lim > 0; l++) {
       long long mx = 0;
       for (int k = 0; k < nslices; k++) mx = std::max(mx, H.lv[l].sptr[k + 1] - H.lv[l].sptr[k]);
-      if (mx <= TAIL_ROWS && L - l <= TAIL_MAXL) {
+      if (mx <= lim && L - l <= TAIL_MAXL) {
         H.tail = l;
         break;
       }
@@ -1207,7 +1218,8 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
              (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1));
   }
   if (H.mode == 0 && H.tail > 0) {
-    int cl = std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
+    int cl = TAIL_CL > 0 ? std::min(TAIL_CL, TAIL_MAXCL)
+                         : std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
     launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(TAIL_BS), 0, cl, (const TailArgs*)H.tail_args.p, active);
   } else if (H.tail > 0) {
     launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p);
