@@ -49,6 +49,16 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- helpers
+def max_over_ranks(t, dist=None, device=None):
+    """The job's time = the slowest rank's device time (contract: max over ranks)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(t)
+    import torch
+    tt = torch.tensor([float(t)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
 def hbm_peak():
     try:
         return float(json.load(open(PEAKS_FILE))["hbm_gbs"]), "measured"
@@ -256,11 +266,7 @@ def main():
     if dist is not None:
         dist.barrier()
     clocks = clk.stop()
-    t = e0.elapsed_time(e1) / 1e3
-    if dist is not None:
-        tt = torch.tensor([t], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
+    t = max_over_ranks(e0.elapsed_time(e1) / 1e3, dist, dev)
     value = world * args.steps / t
     st = last["st"]
 
@@ -283,11 +289,7 @@ def main():
         step_e2e()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    te = e0.elapsed_time(e1) / 1e3
-    if dist is not None:
-        tt = torch.tensor([te], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
+    te = max_over_ranks(e0.elapsed_time(e1) / 1e3, dist, dev)
     io_bytes = 8 * (ctx.n + 2 * ctx.m)
 
     # ---- per-kernel shares: one extra step of the same system issued eagerly (the
@@ -314,10 +316,11 @@ def main():
             avg_s = ms / cnt / 1e3
             model = models[_match_model(name, models)]
             ach = model / avg_s / 1e9
-            traffic = None
+            traffic = None       # DRAM bytes per launch from the committed ncu --set full capture
             try:
-                summ = json.load(open(NCU_SUMMARY))
-                traffic = summ.get("dram_bytes_per_launch", {}).get(_match_model(name, models))
+                summ = json.load(open(NCU_SUMMARY))["dram_bytes_per_launch"][args.config]
+                short = _match_model(name, models).replace("bbot::", "").replace("void ", "")
+                traffic = next((v for k, v in summ.items() if k.replace("void ", "") == short), None)
             except Exception:
                 pass
             roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
