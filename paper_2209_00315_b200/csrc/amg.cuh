@@ -1,16 +1,18 @@
-// amg.cuh -- I3: device pairwise-aggregation AMG (the role of AGMG).
+// amg.cuh -- I3: device aggregation AMG (the role of AGMG).
 //
 // The algorithm is the build's own, deterministic definition (DESIGN.md §2 I3,
-// identical to oracle/amg.py): strength |a_ij| within a time slice; 16
-// synchronous rounds of mutual-strongest-neighbour matching with near-ties
-// (relative 1e-8) broken towards the lower index; two passes per level
-// (aggregates <= 4 rows); piecewise-constant prolongation; Galerkin coarse
-// operators; damped-Jacobi V(1,1); coarsest: per-slice grounded dense inverse
-// (mode A, singular Laplacians) or one dense inverse (mode T).
+// identical to oracle/amg.py): strength (|a_ij| + |a_ji|)/2 within a time slice;
+// 16 synchronous rounds of mutual-strongest-neighbour matching, near-ties
+// (relative 1e-8) broken by a fixed hash priority; leftover rows attached to the
+// pair of their strongest matched neighbour; two passes per level;
+// piecewise-constant prolongation; Galerkin coarse operators; damped-Jacobi
+// V(1,1); K-cycle coarse corrections on deep AMG(A) hierarchies; coarsest:
+// per-slice grounded dense inverse (mode A, singular Laplacians) or one dense
+// inverse (mode T).
 //
 // Level 0 is never materialised as CSR: it is read through a "view" -- the
-// edge-weight form of the blocks A_k (EdgeLapView) or the slice-shared ELL of T
-// (SliceEllView).  Coarse levels are CSR (int64 row pointers).
+// cell-ELL form of the blocks A_k (LapView) or the slice-shared ELL of T
+// (SliceEllView).  Coarse levels: CSR for setup, SELL-32 for the sweeps.
 #pragma once
 #include "common.cuh"
 #include "pcg_fin.cuh"
