@@ -42,6 +42,7 @@ typedef enum {
   BBOT_E_STATE = 3,     /* rho <= 0 or s <= 0 in a state (IPM interior)           */
   BBOT_E_NOCONV = 4,    /* reserved (non-convergence is reported in stats, not here)     */
   BBOT_E_CUDA = 5,      /* CUDA runtime error (message has the CUDA string)              */
+  BBOT_E_NCCL = 6,      /* NCCL error or libnccl.so.2 not loadable                       */
   BBOT_E_NOMEM = 7,     /* device allocation failed                                     */
   BBOT_E_INTERNAL = 8,  /* internal capacity exceeded (AMG row too wide) / bug           */
   BBOT_E_ORDER = 9      /* call order (e.g. solve before assemble)                      */
@@ -191,6 +192,24 @@ bbot_status bbot_amg_vcycle(bbot_ctx* ctx, int which, const double* b, double* x
  * (kernels replayed from the solve's CUDA graph are not counted; run the same
  * solve with bbot_set_exec_mode(ctx, 0) or under the profiler to count them). */
 long long bbot_launch_count(const bbot_ctx* ctx);
+/* Multi-GPU time slabs, one process per GPU.
+ * Rank r owns a contiguous slab [k_begin, k_end) of the K+1 potential slices
+ * (sizes differ by at most one).  The per-slice A_k solves of every BB apply
+ * ((4.20), P:1469 -- independent per time slice) run on the owned slices
+ * only and are then exchanged with NCCL (one grouped broadcast per slab, on the
+ * context stream, inside the apply); every other step is computed redundantly and
+ * deterministically on all ranks, so every rank holds the same iterate, bitwise
+ * equal to the single-GPU run.  Multi-rank solves are issued eagerly (NCCL is not
+ * captured into the conditional-node solve graph).  Inner-A statistics become
+ * per-rank.  Memory is NOT divided by the rank count in this scope.
+ * bbot_nccl_unique_id: on rank 0; the caller broadcasts the 128 bytes.
+ * bbot_set_dist: after bbot_create, before bbot_assemble; uid == NULL makes a
+ * "virtual rank" (the partition without communication: non-owned slices of the
+ * A_k solutions stay 0) for testing the partition on one GPU. */
+bbot_status bbot_nccl_unique_id(unsigned char out[128]);
+bbot_status bbot_set_dist(bbot_ctx* ctx, int rank, int nranks, const unsigned char* uid);
+bbot_status bbot_get_slab(const bbot_ctx* ctx, int* k_begin, int* k_end);
+
 /* Execution mode of bbot_solve.  1 (default): the whole solve -- FGMRES, the BB
  * applies with their inner GMRES / per-slice PCG loops, recovery -- is captured
  * once per bbot_assemble into one CUDA graph whose loops are conditional WHILE

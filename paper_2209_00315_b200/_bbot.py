@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libbbot.so")
 
 BBOT_MEM_HOST, BBOT_MEM_DEVICE = 0, 1
 STATUS = {0: "OK", 1: "E_INPUT", 2: "E_GEOMETRY", 3: "E_STATE", 4: "E_NOCONV", 5: "E_CUDA",
-          7: "E_NOMEM", 8: "E_INTERNAL", 9: "E_ORDER"}
+          6: "E_NCCL", 7: "E_NOMEM", 8: "E_INTERNAL", 9: "E_ORDER"}
 
 
 class SolverOpts(C.Structure):
@@ -94,6 +94,9 @@ _sigs = {
     "bbot_amg_vcycle": (C.c_int, [_P, C.c_int, _P, _P, C.c_int]),
     "bbot_launch_count": (C.c_longlong, [_P]),
     "bbot_set_exec_mode": (C.c_int, [_P, C.c_int]),
+    "bbot_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "bbot_set_dist": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
+    "bbot_get_slab": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bbot_prof_start": (C.c_int, [_P]),
     "bbot_prof_stop": (C.c_int, [_P, C.c_char_p, C.c_longlong, C.POINTER(C.c_longlong)]),
 }
@@ -109,6 +112,14 @@ class BbotError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib.bbot_nccl_unique_id(buf)
+    if st != 0:
+        raise BbotError(st, "bbot_nccl_unique_id failed (see stderr)")
+    return buf.raw
 
 
 def default_solver_opts(**kw) -> SolverOpts:
@@ -309,6 +320,18 @@ class Context:
 
     def launch_count(self):
         return lib.bbot_launch_count(self._h)
+
+    def set_dist(self, rank: int, nranks: int, uid: bytes | None):
+        """Time-slab partition of the A_k solves (uid: 128 bytes from nccl_unique_id() on
+        rank 0, or None for a virtual rank without communication)."""
+        if uid is not None and len(uid) != 128:
+            raise ValueError("uid must be 128 bytes")
+        self._check(lib.bbot_set_dist(self._h, int(rank), int(nranks), uid))
+
+    def slab(self):
+        a, b = C.c_int(), C.c_int()
+        self._check(lib.bbot_get_slab(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_exec_mode(self, use_graph: bool):
         """True: each solve is one CUDA-graph launch (device-side loops); False: eager."""

@@ -149,6 +149,7 @@ void bbot_destroy(bbot_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->dev.stream);
   drop_solve_graph(c);
+  drop_dist(c);
   delete c;
 }
 
@@ -430,6 +431,31 @@ bbot_status bbot_amg_vcycle(bbot_ctx* c, int which, const double* b, double* x, 
 }
 
 long long bbot_launch_count(const bbot_ctx* c) { return c ? c->dev.launches : 0; }
+
+bbot_status bbot_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return BBOT_E_INPUT;
+  try {
+    nccl_unique_id(out);
+  } catch (const Error& e) {
+    fprintf(stderr, "bbot_nccl_unique_id: %s\n", e.what());
+    return e.status;
+  }
+  return BBOT_OK;
+}
+
+bbot_status bbot_set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid) {
+  if (!c) return BBOT_E_INPUT;
+  API_BEGIN(c)
+  set_dist(c, rank, nranks, uid);
+  API_END(c)
+}
+
+bbot_status bbot_get_slab(const bbot_ctx* c, int* k_begin, int* k_end) {
+  if (!c) return BBOT_E_INPUT;
+  if (k_begin) *k_begin = c->nranks > 1 ? c->own_begin : 0;
+  if (k_end) *k_end = c->nranks > 1 ? c->own_end : c->g.K + 1;
+  return BBOT_OK;
+}
 
 bbot_status bbot_set_exec_mode(bbot_ctx* c, int use_graph) {
   if (!c) return BBOT_E_INPUT;

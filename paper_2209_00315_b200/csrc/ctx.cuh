@@ -98,6 +98,10 @@ struct bbot_ctx {
   bbot::DBuf<double> scal;      // device scalars / per-slice scratch (>= 8*(K+2))
   bbot::DBuf<long long> scan_ws;
   bbot::DBuf<double> nrm_T;      // ||r2|| of the current BB apply (device scalar)
+  // multi-GPU time slabs (dist.cu): owned potential slices [own_begin, own_end)
+  int rank = 0, nranks = 1, own_begin = 0, own_end = 1 << 30;
+  bool virt = false;             // virtual rank (no communication; partition tests on one GPU)
+  void* comm = nullptr;          // ncclComm_t
   long long n() const { return (long long)g.N * (g.K + 1); }
   long long m() const { return (long long)g.nbar * g.K; }
 };

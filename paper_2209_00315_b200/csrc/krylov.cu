@@ -319,7 +319,7 @@ void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, con
 
 // ------------------------------------------------------------ per-slice PCG
 __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,
-                            PcgScal* P, int maxit, RedArgs R) {
+                            PcgScal* P, int maxit, RedArgs R, int own_begin, int own_end) {
   int k = blockIdx.y;
   const int ns = gridDim.y;
   long long beg, end;
@@ -338,10 +338,11 @@ __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* _
     double bn = sqrt(R.out[q]);
     s[PS_BN * ns + q] = bn;
     s[PS_RN * ns + q] = bn;
-    s[PS_ACTIVE * ns + q] = bn > 0.0 ? 1.0 : 0.0;
+    const bool act = bn > 0.0 && q >= own_begin && q < own_end;   // other ranks' slices never iterate
+    s[PS_ACTIVE * ns + q] = act ? 1.0 : 0.0;
     s[PS_BETA * ns + q] = 0.0;
     its[q] = 0;
-    if (bn > 0.0) atomicOr(&any, 1);
+    if (act) atomicOr(&any, 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {

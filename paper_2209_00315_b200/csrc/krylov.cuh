@@ -63,9 +63,11 @@ struct DevPcg {
   // pre(r, z, fuse): z = M r; if fuse != nullptr the preconditioner must also
   // emit the per-slice reduction r.z with fuse's epilogue (fused into its last
   // kernel), else the PCG launches it separately.
+  // Only slices in [own_begin, own_end) iterate (multi-GPU time slabs: the others
+  // are some other rank's; they are skipped by every kernel and x is left as 0).
   template <class V, class Pre>
   void emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const double* b, double* x,
-            long long slice_len, double tol, int maxit);
+            long long slice_len, double tol, int maxit, int own_begin = 0, int own_end = 1 << 30);
   void reset_stats(Dev& d);
 };
 
@@ -78,7 +80,7 @@ void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n,
 
 // r = b, bn = ||b^k||, active = bn > 0, its = 0, it = 0; loop flag = any active
 __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,
-                            PcgScal* P, int maxit, RedArgs R);
+                            PcgScal* P, int maxit, RedArgs R, int own_begin, int own_end);
 // rz_new = r.z; beta (it > 0) and rz update
 __global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, RedArgs R,
                          PcgRzFin fin);
@@ -113,7 +115,7 @@ __global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double*
 
 template <class V, class Pre>
 void DevPcg::emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const double* b, double* x,
-                  long long L, double tol, int maxit) {
+                  long long L, double tol, int maxit, int own_begin, int own_end) {
   const int ns = nslices;
   const int BS = Reducer::BS;
   int parts = red.parts_for(L, ns);
@@ -123,7 +125,7 @@ void DevPcg::emit(Dev& d, Reducer& red, const V& view, const Pre& pre, const dou
   BB_CUDA(cudaMemsetAsync(p.p, 0, n * sizeof(double), d.stream));
   BB_CUDA(cudaMemsetAsync(q.p, 0, n * sizeof(double), d.stream));
   launch(d, k_pcg_start, dim3(parts, ns), dim3(BS), 0, L, b, r.p, S, its.p, sc.p, maxit,
-         red.args(parts, ns, out));
+         red.args(parts, ns, out), own_begin, own_end);
   dev_while(d, dev_field(sc.p, &PcgScal::flag), [&](const LoopCtl& ctl) {
     SliceDotFuse fz{red.args(parts, ns, out), parts, ns, L, PcgRzFin{S, sc.p, ns}, S + PS_ACTIVE * ns};
     if (!pre(r.p, z.p, &fz))

@@ -31,4 +31,11 @@ void bb_apply(bbot_ctx* c, const double* r, double* z, int* its_T, int* its_A_ma
 void solve(bbot_ctx* c, bbot_solve_stats* st);                                          // graph (or eager)
 void drop_solve_graph(bbot_ctx* c);
 
+// dist.cu
+int slab_begin(int nslices, int rank, int nranks);
+void nccl_unique_id(unsigned char out[128]);
+void set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid);
+void drop_dist(bbot_ctx* c);
+void exchange_slabs(bbot_ctx* c, double* x);   // every rank's slab of [K+1][N] to every rank
+
 }  // namespace bbot

@@ -102,7 +102,8 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
       [&](const double* x, double* y, const SliceDotFuse* f) {
         return amg_vcycle(c->dev, c->amgA, vA, x, y, f, f ? f->active : nullptr);
       },
-      c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner);
+      c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner, c->own_begin, c->own_end);
+  exchange_slabs(c, z1);        // multi-GPU: every rank's A_k solutions to every rank (dist.cu)
   remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
 }
 
@@ -122,7 +123,8 @@ static void emit_solve(bbot_ctx* c) {
 template <class Emit>
 static void run_emitted(bbot_ctx* c, cudaGraphExec_t* cache, Emit&& emit) {
   Dev& d = c->dev;
-  bool graph = c->use_graph && !d.prof && cache != nullptr;
+  // NCCL inside conditional-node graphs is not relied on: multi-rank solves run eagerly
+  bool graph = c->use_graph && !d.prof && cache != nullptr && c->comm == nullptr;
   c->t_capture_ms = 0;
   if (!graph) {
     emit();
