@@ -5,6 +5,7 @@
 #include "amg.cuh"
 #include <climits>
 #include <cooperative_groups.h>
+#include <chrono>
 namespace cg = cooperative_groups;
 
 namespace bbot {
@@ -692,6 +693,7 @@ __global__ void k_csr_to_dense(CsrView A, int n, double* D, double* I) {
 // At the end pivot row piv[p] holds D[piv[p]][p] e_p^T | (that multiple of row p
 // of the inverse): inv[p][:] = I[piv[p]][:] / D[piv[p]][p].
 constexpr int GJ_BS = 256;
+constexpr int GJ_MAXOWN = 1024;         // rows per block (n <= 8192, >= 8 blocks)
 __global__ void __launch_bounds__(GJ_BS) k_gj_coop(int n, double* D, double* I, double* cand_v, int* cand_i,
                                                     int* used, int* piv, double* out) {
   cg::grid_group grid = cg::this_grid();
@@ -699,6 +701,7 @@ __global__ void __launch_bounds__(GJ_BS) k_gj_coop(int n, double* D, double* I, 
   __shared__ double sv[GJ_BS];
   __shared__ int si[GJ_BS];
   __shared__ int s_piv;
+  __shared__ double fs[GJ_MAXOWN];      // multipliers of the rows this block owns
   // rows owned by this block: i = blockIdx.x + q*nb
   auto propose = [&](int col) {
     double best = -1.0;
@@ -728,30 +731,48 @@ __global__ void __launch_bounds__(GJ_BS) k_gj_coop(int n, double* D, double* I, 
   propose(0);
   grid.sync();
   for (int p = 0; p < n; p++) {
-    if (tid == 0) {   // every block reduces the candidates identically
+    if (tid < 32) {   // every block reduces the candidates identically (warp, fixed order)
       double best = -1.0;
       int bi = INT_MAX;
-      for (int b = 0; b < nb; b++) {
+      for (int b = tid; b < nb; b += 32) {
         double v = cand_v[(p & 1) * nb + b];
         int i = cand_i[(p & 1) * nb + b];
         if (v > best || (v == best && i < bi)) { best = v; bi = i; }
       }
-      s_piv = bi;
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_down_sync(0xffffffffu, best, o);
+        int i2 = __shfl_down_sync(0xffffffffu, bi, o);
+        if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+      }
+      if (tid == 0) s_piv = bi;
     }
     __syncthreads();
     const int pr = s_piv;
     const double pv = D[(size_t)pr * n + p];
-    // eliminate column p from every other row owned by this block
-    for (int i = blockIdx.x; i < n; i += nb) {
-      if (i == pr) continue;
-      double f = D[(size_t)i * n + p] / pv;
-      if (f == 0.0) continue;
-      for (int j = tid; j < n; j += GJ_BS) {
-        if (j > p) D[(size_t)i * n + j] -= f * D[(size_t)pr * n + j];
-        I[(size_t)i * n + j] -= f * I[(size_t)pr * n + j];
+    // eliminate column p from every other row owned by this block: all multipliers
+    // first (one barrier), then the (row, column) updates as one flat loop
+    const int nown = (n - 1 - (int)blockIdx.x) / nb + 1;     // rows i = blockIdx.x + q*nb
+    for (int q = tid; q < nown; q += GJ_BS) {
+      int i = blockIdx.x + q * nb;
+      fs[q] = (i == pr) ? 0.0 : D[(size_t)i * n + p] / pv;
+    }
+    __syncthreads();
+    {   // warp per owned row, lanes over columns (coalesced, independent iterations)
+      const int lane = tid & 31, wp = tid >> 5, nw = GJ_BS / 32;
+      const double* Dp = D + (size_t)pr * n;
+      const double* Ip = I + (size_t)pr * n;
+      for (int q = wp; q < nown; q += nw) {
+        const double f = fs[q];
+        if (f == 0.0) continue;                       // warp-uniform
+        double* Di = D + (size_t)(blockIdx.x + q * nb) * n;
+        double* Ii = I + (size_t)(blockIdx.x + q * nb) * n;
+#pragma unroll 4
+        for (int j = lane; j < n; j += 32) {
+          double dv = j > p ? Di[j] - f * Dp[j] : (j == p ? 0.0 : Di[j]);
+          Di[j] = dv;
+          Ii[j] -= f * Ip[j];
+        }
       }
-      __syncthreads();
-      if (tid == 0) D[(size_t)i * n + p] = 0.0;
     }
     if (tid == 0 && blockIdx.x == 0) piv[p] = pr;
     if (blockIdx.x == pr % nb && tid == 0) used[pr] = 1;
@@ -959,6 +980,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     BB_CUDA(cudaMemcpyAsync(L0.slice_of.p, slice0, L0.n * sizeof(int), cudaMemcpyDeviceToDevice, s));
   }
   Sg sg;
+  const bool timing = getenv("BBOT_TIMING") != nullptr;
+  auto t_lv = std::chrono::steady_clock::now();
   for (int l = 0;; l++) {
     long long n = H.lv[l].n;
     {
@@ -1006,6 +1029,10 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     }
     H.lv.push_back(std::move(next));
     sync(d);  // temporaries (A1, agg1, ...) are freed stream-ordered; keep host state simple
+    if (timing)
+      fprintf(stderr, "[bbot]   amg mode %d level %d (%lld rows): %.2f ms\n", mode, l, n,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lv).count());
+    t_lv = std::chrono::steady_clock::now();
   }
   // coarsest
   AmgLevel& C = H.lv.back();
@@ -1047,7 +1074,10 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     launch(d, k_csr_to_dense, dim3(nblocks(n, BS)), dim3(BS), 0, C.view(), (int)n, D.p, Iw.p);
     int per_sm = 0;
     BB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, GJ_BS, 0));
-    int nbk = std::max(1, std::min(per_sm * d.num_sms, (int)std::min<long long>(n, 2 * d.num_sms)));
+    // few blocks: each pivot step is latency-bound (candidate reduction + one grid
+    // barrier), and the elimination of an n <= 1024 system needs little parallelism
+    int nbk = std::max(1, std::min(per_sm * d.num_sms, (int)std::min<long long>((n + 7) / 8, 128)));
+    nbk = std::max(nbk, (int)((n + GJ_MAXOWN - 1) / GJ_MAXOWN));
     cv.alloc(2 * (size_t)nbk, s);
     ci.alloc(2 * (size_t)nbk, s);
     used.alloc(n, s);
@@ -1114,6 +1144,11 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
   // hierarchies run every level as graph-replayed grid kernels, which measured faster on
   // C2 than any in-kernel fusion of the coarse levels (172.8 vs 185-299 ms per step),
   // unless BBOT_TAIL_ROWS asks for a tail.
+  if (timing) {
+    sync(d);
+    fprintf(stderr, "[bbot]   amg mode %d coarsest (%lld rows) + SELL: %.2f ms\n", mode, H.lv.back().n,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lv).count());
+  }
   if (mode == 0) H.tail = 0;
   if (mode == 0 && H.lv.size() >= 2) {
     int L = (int)H.lv.size();

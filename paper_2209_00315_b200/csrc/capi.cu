@@ -108,6 +108,8 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
     }
     BB_CUDA(cudaDeviceGetAttribute(&c->dev.num_sms, cudaDevAttrMultiProcessorCount, devid));
     c->red.init(&c->dev, std::max(K + 2, 64));
+    BB_CUDA(cudaStreamCreateWithFlags(&c->dev2.stream, cudaStreamNonBlocking));
+    c->dev2.num_sms = c->dev.num_sms;
     if (const char* e = getenv("BBOT_EAGER")) c->use_graph = (atoi(e) == 0);
     if (const char* e = getenv("BBOT_SYNC_CHECK")) c->dev.sync_check = (atoi(e) != 0);
     for (int i = 0; i < nt; i++)
@@ -150,7 +152,10 @@ void bbot_destroy(bbot_ctx* c) {
   cudaStreamSynchronize(c->dev.stream);
   drop_solve_graph(c);
   drop_dist(c);
+  cudaStream_t s2 = c->dev2.stream;
+  if (s2) cudaStreamSynchronize(s2);
   delete c;
+  if (s2) cudaStreamDestroy(s2);
 }
 
 const char* bbot_last_error(const bbot_ctx* c) { return c ? c->err.c_str() : "null context"; }

@@ -82,6 +82,9 @@ struct bbot_ctx {
   bbot::Assembled as;
   bbot::AmgHierarchy amgA, amgT;
   bbot::AmgWork amgw;
+  // AMG(T) is set up concurrently with AMG(A): its own stream + host thread (solver.cu)
+  bbot::Dev dev2;
+  bbot::AmgWork amgw2;
   // direction
   bool have_dir = false;
   bbot::DBuf<double> sol, dphi, drho, ds;

@@ -7,6 +7,8 @@
 // eagerly with the host reading the loop flags.
 #include "ops.cuh"
 #include <chrono>
+#include <exception>
+#include <thread>
 
 namespace bbot {
 
@@ -51,8 +53,51 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   double ta = t0.ms();
   EvTimer t1(c->dev.stream);
   AmgWork& w = c->amgw;
-  amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
-  amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
+  if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
+    amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
+    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
+  } else {
+    // The two setups are independent and host-latency-bound (size read-backs between
+    // kernels): AMG(T) runs on a second stream from a second host thread, after the
+    // assembly on the main stream; the main stream then waits for it.
+    cudaEvent_t ready, done;
+    BB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    BB_CUDA(cudaEventRecord(ready, c->dev.stream));
+    BB_CUDA(cudaStreamWaitEvent(c->dev2.stream, ready, 0));
+    c->dev2.sync_check = c->dev.sync_check;
+    std::exception_ptr err;
+    double tT = 0, tA = 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    std::thread th([&]() {
+      try {
+        auto a = now();
+        amg_setup(c->dev2, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, c->amgw2);
+        sync(c->dev2);
+        tT = std::chrono::duration<double, std::milli>(now() - a).count();
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      auto a = now();
+      amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
+      sync(c->dev);
+      tA = std::chrono::duration<double, std::milli>(now() - a).count();
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (getenv("BBOT_TIMING")) fprintf(stderr, "[bbot] setup AMG(A) %.2f ms, AMG(T) %.2f ms (concurrent)\n", tA, tT);
+    if (err) std::rethrow_exception(err);
+    BB_CUDA(cudaEventRecord(done, c->dev2.stream));
+    BB_CUDA(cudaStreamWaitEvent(c->dev.stream, done, 0));
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+    c->dev.launches += c->dev2.launches;
+    c->dev2.launches = 0;
+  }
   double ts = t1.ms();
   c->as.valid = true;
   c->t_assemble_ms = ta;
