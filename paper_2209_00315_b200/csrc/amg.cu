@@ -287,6 +287,40 @@ __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, con
 
 
 
+// pre-smoothing x = om D^-1 b first, then the residual sweep reads x (same
+// expression order as k_down: bitwise identical), one gather per entry
+__global__ void k_jacobi0(long long n, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                          double* __restrict__ x) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) x[r] = om * dinv[r] * b[r];
+}
+template <class V>
+__global__ void k_resid(V v, const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ res) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= v.nrows) return;
+  double acc = b[r];
+  v.row(r, [&](long long c, double a) { acc -= a * x[c]; });
+  res[r] = acc;
+}
+
+// xp = x + P xc (prolongated coarse correction), then the post-smoothing sweep on xp:
+// two launches instead of k_up's chained gathers (neighbour -> agg -> xc) on each of
+// T's ~27 entries per row; the same sums in the same order (bitwise identical)
+__global__ void k_prolong(long long n, const double* __restrict__ x, const int* __restrict__ agg,
+                          const double* __restrict__ xc, double* __restrict__ xp) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) xp[r] = x[r] + xc[agg[r]];
+}
+template <class V>
+__global__ void k_post(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                       const double* __restrict__ xp, double* __restrict__ xo) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= v.nrows) return;
+  double acc = b[r];
+  v.row(r, [&](long long c, double a) { acc -= a * xp[c]; });
+  xo[r] = xp[r] + om * dinv[r] * acc;
+}
+
 template <class V>
 __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
                      const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
@@ -1243,7 +1277,10 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
   for (int l = 0; l < stop; l++) {
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
-    if (l == 0)
+    if (l == 0 && H.mode == 1) {   // T level 0: Jacobi step first, then a plain residual sweep
+      launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p);
+      launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p);
+    } else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0));
     else
       launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
@@ -1269,6 +1306,9 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     if (l == 0 && fuse) {
       launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);
+    } else if (l == 0 && H.mode == 1) {   // T level 0: prolongate first, then a plain sweep
+      launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p);
+      launch(d, k_post<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.xt.p, out);
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
              (const int*)lv.agg.p, xc, out, skip_at(0));
