@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--scale-config", default="C4", help="HBM-bound size reported beside the headline ('' = none)")
     ap.add_argument("--profile-out", default=None, help="write the per-kernel table (json) here")
     return ap.parse_args()
 
@@ -208,6 +209,77 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def roofline_of(ctx, prof_table, config):
+    """Roofline object for the dominant kernel with a byte model, from one eagerly
+    issued step's per-launch CUDA-event table."""
+    nnzT, _ = ctx.T_nnz()
+    models = byte_models(ctx, nnzT)
+    total_ms = sum(v[1] for v in prof_table.values())
+    ranked = sorted(prof_table.items(), key=lambda kv: -kv[1][1])
+    dom = next(((k, v) for k, v in ranked if _match_model(k, models)), None)
+    peak, peak_kind = hbm_peak()
+    roof = None
+    if dom is not None:
+        name, (cnt, ms) = dom
+        avg_s = ms / cnt / 1e3
+        model = models[_match_model(name, models)]
+        ach = model / avg_s / 1e9
+        traffic = None       # DRAM bytes per launch from the committed ncu --set full capture
+        try:
+            summ = json.load(open(NCU_SUMMARY))["dram_bytes_per_launch"][config]
+            short = _match_model(name, models).replace("bbot::", "").replace("void ", "")
+            traffic = next((v for k, v in summ.items() if k.replace("void ", "") == short), None)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": model, "avg_launch_us": round(avg_s * 1e6, 2),
+                "launches_per_step": cnt, "share_of_step": round(ms / total_ms, 4),
+                "top_kernel": ranked[0][0], "top_kernel_share": round(ranked[0][1][1] / total_ms, 4)}
+    return roof, ranked, total_ms, models
+
+
+def scale_point(pb, config, dev, stream, steps=2):
+    """The same step on the largest single-GPU config (C4: 67.5 M unknowns, vectors of
+    0.4-0.5 GB, HBM-bound) -- reported beside the headline line, not instead of it."""
+    import torch
+    from synthetic import initial_state, make_problem
+    p = make_problem(config)
+    phi, rho, s = initial_state(p, 1.0)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream)
+    xs = [torch.tensor(x, device=dev) for x in (phi, rho, s)]
+    last = {}
+
+    def step():
+        ctx.set_state(*xs, 1.0)
+        ctx.assemble()
+        last["st"] = ctx.solve_stats_only()
+        ctx.newton_update(0.95)
+
+    step()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3 / steps
+    ctx.prof_start()
+    step()
+    roof, _, _, _ = roofline_of(ctx, ctx.prof_stop(), config)
+    st = last["st"]
+    out = {"workload": f"{config}: first IPM Newton system (A19 point, mu=1), eps_out=1e-10", "nbar": ctx.nbar,
+           "K": ctx.K, "n_plus_m": ctx.n + ctx.m, "value": 1.0 / t, "unit": "solves/s", "ms_per_step": 1e3 * t,
+           "unknowns_per_s": (ctx.n + ctx.m) / t, "steps": steps, "warmup": 1,
+           "solve": {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "inner_A_its_total",
+                                        "converged", "rel_res")},
+           "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms")},
+           "roofline": roof}
+    ctx.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -311,32 +383,17 @@ def main():
         step()
         prof_table = ctx.prof_stop()
         launches = ctx.launch_count() - l0
-        nnzT, _ = ctx.T_nnz()
-        models = byte_models(ctx, nnzT)
-        total_ms = sum(v[1] for v in prof_table.values())
-        ranked = sorted(prof_table.items(), key=lambda kv: -kv[1][1])
-        dom = next(((k, v) for k, v in ranked if _match_model(k, models)), None)
-        peak, peak_kind = hbm_peak()
-        if dom is not None:
-            name, (cnt, ms) = dom
-            avg_s = ms / cnt / 1e3
-            model = models[_match_model(name, models)]
-            ach = model / avg_s / 1e9
-            traffic = None       # DRAM bytes per launch from the committed ncu --set full capture
-            try:
-                summ = json.load(open(NCU_SUMMARY))["dram_bytes_per_launch"][args.config]
-                short = _match_model(name, models).replace("bbot::", "").replace("void ", "")
-                traffic = next((v for k, v in summ.items() if k.replace("void ", "") == short), None)
-            except Exception:
-                pass
-            roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                    "algorithmic_bytes_per_launch": model, "avg_launch_us": round(avg_s * 1e6, 2),
-                    "launches_per_step": cnt, "share_of_step": round(ms / total_ms, 4),
-                    "top_kernel": ranked[0][0], "top_kernel_share": round(ranked[0][1][1] / total_ms, 4)}
+        roof, ranked, total_ms, models = roofline_of(ctx, prof_table, args.config)
         if args.profile_out and rank == 0:
             json.dump({"config": args.config, "kernels": {k: {"launches": v[0], "ms": v[1]} for k, v in ranked},
                        "total_ms": total_ms, "models": models}, open(args.profile_out, "w"), indent=1)
+
+    scale = None
+    if rank == 0 and world == 1 and args.scale_config and args.scale_config != args.config and not args.no_profile:
+        try:
+            scale = scale_point(pb, args.scale_config, dev, stream)
+        except Exception as ex:                          # the headline line must still print
+            scale = {"error": str(ex)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -367,6 +424,7 @@ def main():
             "gpu_launches": int(launches) if launches is not None else None,
             "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms", "t_graph_ms")},
             "roofline": roof,
+            "hbm_scale_point": scale,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
