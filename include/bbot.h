@@ -60,7 +60,7 @@ typedef struct {
   int restart_T;       /* inner GMRES restart [10], 1..32                                   */
   int maxit_inner;     /* inner caps (T GMRES total its, per-slice PCG its) [50]            */
   double omega_A;      /* damped-Jacobi weight, AMG(A) [2/3]                                */
-  double omega_T;      /* damped-Jacobi weight, AMG(T) [0.7]                                */
+  double omega_T;      /* damped-Jacobi weight, AMG(T) [0.5] (< 2/max Re lambda(D^-1 T), I3)  */
   int coarse_max_A;    /* AMG(A) coarsest: max rows per time slice [64]                     */
   int coarse_max_T;    /* AMG(T) coarsest: max rows in total [1024]                         */
 } bbot_solver_opts;

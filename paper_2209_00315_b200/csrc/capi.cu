@@ -64,7 +64,7 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->restart_T = 10;
   o->maxit_inner = 50;
   o->omega_A = 2.0 / 3.0;
-  o->omega_T = 0.7;
+  o->omega_T = 0.5;
   o->coarse_max_A = 64;
   o->coarse_max_T = 1024;
 }

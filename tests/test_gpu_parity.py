@@ -278,6 +278,30 @@ def test_ipm_parity_T2_full():
     _ipm_compare(log, res.log, st, res.kinetic_energy)
 
 
+def test_ipm_parity_C1_full():
+    """The BASELINE configs[0] protocol itself: full IPM on C1 (512 cells, K = 8),
+    mu 1 -> 2^-26 ~ 1.49e-8 (A17-A20), against the oracle's own run stored in
+    tests/golden/ipm_C1.json (written by scripts/oracle_ipm_golden.py, which calls
+    only oracle/; ~10 min on one core).  Same systems, trajectory, final kinetic
+    energy to 1e-6 (north star).  The systems that run to the 400 cap on both sides
+    are the last Newton step of each mu, where ||F|| is already ~1e-9..1e-11 and
+    eps = 1e-10 relative to it is below fp64 resolution."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "ipm_C1.json")
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated")
+    gold = json.load(open(path))
+    pb = _gpu()
+    p = make_problem("C1")
+    phi, rho, s = initial_state(p, 1.0)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts())
+    assert abs(st["final_mu"] - gold["final_mu"]) <= 1e-15 * gold["final_mu"]
+    _ipm_compare(log, gold["systems"], st, gold["kinetic_energy"])
+
+
 def test_ipm_parity_C1_converging_range():
     """IPM on BASELINE configs[0] (C1: 512 cells, K = 8) over the mu range where the
     BB-preconditioned FGMRES converges, mu 1 -> 2^-9 ~ 1.95e-3 (A17-A20; 36 Newton

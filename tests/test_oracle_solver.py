@@ -187,3 +187,29 @@ def test_bb_counts_vs_table4(L, K, table):
     S = BBSolver(d, phi, rho, s, 1.0, SolverOpts(exact_inner=True, eps_out=1e-5))
     S.solve()
     assert table / 2 <= S.stats["outer_its"] <= 2 * table
+
+
+@pytest.mark.slow
+def test_T_smoother_weight_contracts_on_ipm_path():
+    """I3 reading: the damped-Jacobi weight of AMG(T) must keep omega * max Re
+    lambda(D^-1 T) < 2 along the IPM path (D = diag T).  At mu = 1 the spectrum of
+    D^-1 T lies in (0, 2]; as mu -> 0 it grows (T2 at mu = 2^-13: 2.41; C1 at 1.2e-4:
+    3.09, which makes the former omega = 0.7 an amplifying smoother and AMG(T)
+    diverge).  omega_T = 0.5 stays contractive with margin."""
+    from threadpoolctl import threadpool_limits
+    from oracle.ipm import IpmOpts, ipm_run
+    from oracle.ops import Discretisation
+    from synthetic import initial_state, make_problem
+    p = make_problem("T2")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    T0 = d.T_matrix(phi, rho, s).toarray()
+    ev0 = np.linalg.eigvals(T0 / np.diag(T0)[:, None])
+    assert ev0.real.min() > 0 and ev0.real.max() <= 2.0 + 1e-10
+    with threadpool_limits(1):
+        r = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -13), SolverOpts())
+    T = d.T_matrix(r.phi, r.rho, r.s).toarray()
+    ev = np.linalg.eigvals(T / np.diag(T)[:, None])
+    om = SolverOpts().omega_T
+    assert ev.real.min() > 0 and ev.real.max() > 2.0            # the spectrum has grown
+    assert np.abs(1.0 - om * ev).max() < 1.0                    # the smoother contracts every mode
