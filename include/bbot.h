@@ -60,7 +60,7 @@ typedef struct {
   int restart_T;       /* inner GMRES restart [10], 1..32                                   */
   int maxit_inner;     /* inner caps (T GMRES total its, per-slice PCG its) [50]            */
   double omega_A;      /* damped-Jacobi weight, AMG(A) [2/3]                                */
-  double omega_T;      /* damped-Jacobi weight, AMG(T) [0.5] (< 2/max Re lambda(D^-1 T), I3)  */
+  double omega_T;      /* l1-Jacobi weight, AMG(T) [1.0] (D = sum_j |T_ij|, I3)             */
   int coarse_max_A;    /* AMG(A) coarsest: max rows per time slice [64]                     */
   int coarse_max_T;    /* AMG(T) coarsest: max rows in total [1024]                         */
 } bbot_solver_opts;
@@ -90,6 +90,8 @@ typedef struct {
   double frac_to_boundary;  /* [0.95]  (A20)                                                */
   int newton_max;           /* [30]    Newton steps per mu (A18)                             */
   int max_mu_steps;         /* [0 = all] truncate the mu schedule                           */
+  double mu_tight;          /* [0.3]   below this mu the A_k solves tighten ... (A14')       */
+  double eps_A_tight;       /* [1e-5]  ... to this relative tolerance                        */
 } bbot_ipm_opts;
 
 typedef struct {

@@ -168,7 +168,8 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
     cur, cur_slice = A, np.asarray(slice_of_row, dtype=np.int64)
     while True:
         n = cur.shape[0]
-        lv = Level(A=cur, slice_of_row=cur_slice, dinv=1.0 / cur.diagonal())
+        dg = (np.asarray(abs(cur).sum(axis=1)).ravel() if mode == "T" else cur.diagonal())
+        lv = Level(A=cur, slice_of_row=cur_slice, dinv=1.0 / dg)
         levels.append(lv)
         small = (_slice_sizes(cur_slice, nslices).max() <= coarse_max) if mode == "A" else (n <= coarse_max)
         if small or len(levels) >= max_levels:

@@ -34,7 +34,7 @@ class SolverOpts:
     restart_T: int = 10
     maxit_inner: int = 50
     omega_A: float = 2.0 / 3.0
-    omega_T: float = 0.5          # I3: < 2 / max Re lambda(D^-1 T) along the IPM path (3.09 at mu ~ 1e-4)
+    omega_T: float = 1.0          # I3: l1-Jacobi for AMG(T) (D = row sums of |T|)
     coarse_max_A: int = 64        # rows per slice
     coarse_max_T: int = 1024      # rows in total
     exact_inner: bool = False     # pin mode: exact T solve + exact A_k^+ (no AMG)

@@ -41,7 +41,8 @@ class SolveStats(C.Structure):
 class IpmOpts(C.Structure):
     _fields_ = [("mu0", C.c_double), ("mu_factor", C.c_double), ("mu_min", C.c_double),
                 ("newton_rel_tol", C.c_double), ("newton_abs_floor", C.c_double),
-                ("frac_to_boundary", C.c_double), ("newton_max", C.c_int), ("max_mu_steps", C.c_int)]
+                ("frac_to_boundary", C.c_double), ("newton_max", C.c_int), ("max_mu_steps", C.c_int),
+                ("mu_tight", C.c_double), ("eps_A_tight", C.c_double)]
 
 
 class IpmRecord(C.Structure):

@@ -245,12 +245,17 @@ __global__ void k_galerkin(V v, long long nc, const long long* __restrict__ mptr
   }
 }
 
+// smoother diagonal: mode A the diagonal of the (Laplacian) row; mode T the l1 row
+// sum sum_j |a_ij| (l1-Jacobi, I3: T's diagonal can be negative on real IPM iterates,
+// C2 at mu = 0.25) -- summed in the row's entry order (the oracle sums CSR columns in
+// ascending order; rounding-level differences only)
 template <class V>
-__global__ void k_dinv(V v, double* dinv) {
+__global__ void k_dinv(V v, double* dinv, int l1) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= v.nrows) return;
   double dg = 0.0;
-  v.row(r, [&](long long c, double a) { if (c == r) dg += a; });
+  if (l1) v.row(r, [&](long long c, double a) { dg += fabs(a); });
+  else v.row(r, [&](long long c, double a) { if (c == r) dg += a; });
   dinv[r] = 1.0 / dg;
 }
 
@@ -1025,8 +1030,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
       L.x.alloc(n, s);
       L.r.alloc(n, s);
       L.xt.alloc(n, s);
-      if (l == 0) launch(d, k_dinv<V0>, dim3(nblocks(n, BS)), dim3(BS), 0, v0, L.dinv.p);
-      else launch(d, k_dinv<CsrView>, dim3(nblocks(n, BS)), dim3(BS), 0, L.view(), L.dinv.p);
+      if (l == 0) launch(d, k_dinv<V0>, dim3(nblocks(n, BS)), dim3(BS), 0, v0, L.dinv.p, (int)(mode == 1));
+      else launch(d, k_dinv<CsrView>, dim3(nblocks(n, BS)), dim3(BS), 0, L.view(), L.dinv.p, (int)(mode == 1));
       L.sptr = slice_ptrs(d, L.slice_of.p, n, nslices, w);
     }
     std::vector<long long>& sp = H.lv[l].sptr;

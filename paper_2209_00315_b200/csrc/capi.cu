@@ -64,7 +64,7 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->restart_T = 10;
   o->maxit_inner = 50;
   o->omega_A = 2.0 / 3.0;
-  o->omega_T = 0.5;
+  o->omega_T = 1.0;
   o->coarse_max_A = 64;
   o->coarse_max_T = 1024;
 }
@@ -79,6 +79,8 @@ void bbot_default_ipm_opts(bbot_ipm_opts* o) {
   o->frac_to_boundary = 0.95;
   o->newton_max = 30;
   o->max_mu_steps = 0;
+  o->mu_tight = 0.3;
+  o->eps_A_tight = 1e-5;
 }
 
 bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt, int K, const double* rho_in,
@@ -324,11 +326,20 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
     mus.push_back(mu);
   }
   if (o.max_mu_steps > 0 && (int)mus.size() > o.max_mu_steps) mus.resize(o.max_mu_steps);
+  BB_REQUIRE(o.eps_A_tight > 0, BBOT_E_INPUT, "bad eps_A_tight");
+  const double eps_A0 = c->opts.eps_A;
+  struct Restore {           // the caller's eps_A comes back even if a solve throws
+    double& ref;
+    double val;
+    ~Restore() { ref = val; }
+  } restore{c->opts.eps_A, eps_A0};
   c->mu = o.mu0;
   compute_residual(c, false);
   double F0 = c->as.res_norm;
   for (double mu : mus) {
     c->mu = mu;
+    // A14': tighter A_k solves once mu < mu_tight (the solve graph is re-captured per assembly)
+    c->opts.eps_A = mu >= o.mu_tight ? eps_A0 : std::min(eps_A0, o.eps_A_tight);
     double tol = std::max(o.newton_rel_tol * mu, o.newton_abs_floor) * F0;   // A18
     for (int it = 0; it < o.newton_max; it++) {
       bbot_ipm_record rec;
@@ -349,6 +360,7 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
       if (rec.res_norm <= tol) break;
     }
   }
+  c->opts.eps_A = eps_A0;
   S.final_mu = c->mu;
   S.kinetic_energy = kinetic_energy(c);
   S.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
