@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--scale-config", default="C4", help="HBM-bound size reported beside the headline ('' = none)")
+    ap.add_argument("--ipm-config", default="C1", help="config whose full IPM run is reported ('' = none)")
     ap.add_argument("--profile-out", default=None, help="write the per-kernel table (json) here")
     return ap.parse_args()
 
@@ -280,6 +281,26 @@ def scale_point(pb, config, dev, stream, steps=2):
     return out
 
 
+def ipm_protocol(pb, config, dev):
+    """BASELINE configs[0]'s own protocol on the GPU: the full interior-point run (A17-A20,
+    mu 1 -> 2^-26) -- every Newton system of the trajectory, not just the first."""
+    import torch
+    from synthetic import initial_state, make_problem
+    p = make_problem(config)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(*initial_state(p, 1.0), 1.0)
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    st, log = ctx.ipm_run(pb.default_ipm_opts())
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t
+    ctx.close()
+    return {"workload": f"{config}: full IPM, mu 1 -> 2^-26 (A17-A20), eps_out=1e-10", "n_systems": st["n_systems"],
+            "total_outer": st["total_outer"], "n_capped": st["n_unconverged"], "final_mu": st["final_mu"],
+            "kinetic_energy": st["kinetic_energy"], "wall_s": round(wall, 3),
+            "solves_per_s": st["n_systems"] / wall, "timing": "host wall clock around bbot_ipm_run"}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -395,6 +416,13 @@ def main():
         except Exception as ex:                          # the headline line must still print
             scale = {"error": str(ex)[:200]}
 
+    protocol = None
+    if rank == 0 and world == 1 and args.ipm_config and not args.no_profile:
+        try:
+            protocol = ipm_protocol(pb, args.ipm_config, dev)
+        except Exception as ex:
+            protocol = {"error": str(ex)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_outer = oracle_outer_count(args.config)
@@ -425,6 +453,7 @@ def main():
             "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms", "t_graph_ms")},
             "roofline": roof,
             "hbm_scale_point": scale,
+            "ipm_protocol": protocol,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
