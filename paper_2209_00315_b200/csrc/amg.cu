@@ -6,6 +6,8 @@
 #include <climits>
 #include <cooperative_groups.h>
 #include <chrono>
+#include <memory>
+#include <mutex>
 namespace cg = cooperative_groups;
 
 namespace bbot {
@@ -1143,7 +1145,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     for (int l = 1; l < L - 1; l++)
       if (H.lv[l].n <= TAILT_ROWS && L - l <= TAIL_MAXL) { H.tail = l; break; }
     if (H.tail > 0) {
-      static TailTArgs hostTT;
+      std::unique_ptr<TailTArgs> stage(new TailTArgs());   // per call (no shared static state)
+      TailTArgs& hostTT = *stage;
       AmgLevel& P = H.lv[H.tail - 1];
       hostTT.first = H.tail;
       hostTT.last = L - 1;
@@ -1170,11 +1173,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
       H.tail_args.alloc(sizeof(TailTArgs), s);
       BB_CUDA(cudaMemcpyAsync(H.tail_args.p, &hostTT, sizeof(TailTArgs), cudaMemcpyHostToDevice, s));
       H.tail_cl = 16;
-      static bool attr_done = false;
-      if (!attr_done) {
-        BB_CUDA(cudaFuncSetAttribute(k_tailT, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_done = true;
-      }
+      static std::once_flag attr_once;
+      std::call_once(attr_once, [] { cudaFuncSetAttribute(k_tailT, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); });
       sync(d);
     }
   }
@@ -1200,7 +1200,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
         break;
       }
     }
-    static TailArgs hostT;   // staging (the copy below completes before the sync)
+    std::unique_ptr<TailArgs> stage(new TailArgs());   // staging; the copy completes before the sync below
+    TailArgs& hostT = *stage;
     for (int l = std::max(1, H.tail); H.tail > 0 && l < L; l++) {
       AmgLevel& A = H.lv[l];
       A.dsptr.alloc(nslices + 1, s);

@@ -41,6 +41,16 @@ def test_oracle_defaults_agree_with_library():
         assert getattr(o, f) == getattr(s, f), f
 
 
+def test_oracle_ipm_defaults_agree_with_library():
+    """IPM constants (A17-A20, A14') on both sides."""
+    import paper_2209_00315_b200 as pb
+    from oracle.ipm import IpmOpts
+    o, s = pb.default_ipm_opts(), IpmOpts()
+    for f in ("mu0", "mu_factor", "mu_min", "newton_rel_tol", "newton_abs_floor", "frac_to_boundary", "newton_max",
+              "mu_tight", "eps_A_tight"):
+        assert getattr(o, f) == getattr(s, f), f
+
+
 def test_no_oracle_import_in_product(root):
     """The product package never imports the oracle."""
     pkg = os.path.join(root, "paper_2209_00315_b200")
