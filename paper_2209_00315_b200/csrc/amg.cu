@@ -314,9 +314,31 @@ __global__ void k_resid(V v, const double* __restrict__ b, const double* __restr
 // two launches instead of k_up's chained gathers (neighbour -> agg -> xc) on each of
 // T's ~27 entries per row; the same sums in the same order (bitwise identical)
 __global__ void k_prolong(long long n, const double* __restrict__ x, const int* __restrict__ agg,
-                          const double* __restrict__ xc, double* __restrict__ xp) {
+                          const double* __restrict__ xc, double* __restrict__ xp, SliceSkip sk) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) xp[r] = x[r] + xc[agg[r]];
+  if (r < n && !sk.skip(r)) xp[r] = x[r] + xc[agg[r]];
+}
+
+// AMG(A) level 0 after k_prolong: post-smoothing on xp fused with the per-slice dot
+// b.z (the PCG r.z step) -- k_up_dot's values exactly, one gather level per entry
+template <class V>
+__global__ void k_post_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                           const double* __restrict__ xp, double* __restrict__ xo, long long L, RedArgs R,
+                           PcgRzFin fin, const double* active) {
+  int k = blockIdx.y;
+  long long beg, end;
+  red_chunk(L, R.parts, beg, end);
+  if (active && active[k] == 0.0) end = beg;     // converged slice: nothing to do (partial 0)
+  double dot = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    long long r = (long long)k * L + i;
+    double acc = b[r];
+    v.row(r, [&](long long c, double a) { acc -= a * xp[c]; });
+    double z = xp[r] + om * dinv[r] * acc;
+    xo[r] = z;
+    dot += b[r] * z;
+  }
+  if (red_commit(dot, R)) fin(R.out);
 }
 template <class V>
 __global__ void k_post(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
@@ -462,6 +484,7 @@ static long long tune_env(const char* name, long long dflt) {
 static const long long TAIL_ROWS = tune_env("BBOT_TAIL_ROWS", 0);       // A-tail for shallow hierarchies (0: none)
 static const long long TAILT_ROWS = tune_env("BBOT_TAILT_ROWS", 16384); // first T-tail level: <= rows in total
 static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tail cluster size (0: 148/slices)
+static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
 constexpr int TAIL_MAXL = 24;
@@ -1309,11 +1332,17 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     unsigned nb = nblocks(lv.n, BS);
     double* out = l == 0 ? x : level_out(H, l);
     const double* xc = level_out(H, l + 1);
-    if (l == 0 && fuse) {
+    if (l == 0 && fuse && UP_SPLIT) {     // prolongate first, then the sweep fused with r.z
+      launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p,
+             skip_at(0));
+      launch(d, k_post_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
+             (const double*)lv.xt.p, out, fuse->L, fuse->R, fuse->fin, active);
+    } else if (l == 0 && fuse) {
       launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);
     } else if (l == 0 && H.mode == 1) {   // T level 0: prolongate first, then a plain sweep
-      launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p);
+      launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p,
+             SliceSkip{nullptr, nullptr, 1});
       launch(d, k_post<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.xt.p, out);
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,

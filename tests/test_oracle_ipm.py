@@ -85,3 +85,28 @@ def test_kinetic_energy_translation_closed_form():
         kes.append(r.kinetic_energy)
     err = [abs(k - 0.16) for k in kes]
     assert err[1] < err[0] and err[1] < 0.15 * 0.16 * 1.5, kes
+
+
+def test_inner_tolerance_tightens_below_mu_tight(monkeypatch):
+    """A14': the BB apply's A_k solves use eps_A while mu >= mu_tight and
+    min(eps_A, eps_A_tight) below it."""
+    import oracle.ipm as ipm_mod
+    from oracle.bb import SolverOpts
+    from oracle.ipm import IpmOpts, ipm_run
+    from oracle.ops import Discretisation
+    from synthetic import initial_state, make_problem
+    seen = []
+    real = ipm_mod.newton_step
+
+    def spy(d, phi, rho, s, mu, opts, tau):
+        seen.append((mu, opts.eps_A))
+        return real(d, phi, rho, s, mu, opts, tau)
+    monkeypatch.setattr(ipm_mod, "newton_step", spy)
+    p = make_problem("T0")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    ipm_run(d, phi, rho, s, IpmOpts(max_mu_steps=4), SolverOpts())
+    o, io = SolverOpts(), IpmOpts()
+    assert {m for m, _ in seen} == {1.0, 0.5, 0.25, 0.125}
+    for mu, eps in seen:
+        assert eps == (o.eps_A if mu >= io.mu_tight else min(o.eps_A, io.eps_A_tight))
