@@ -3,6 +3,7 @@
 // block of a fused reduction; the host only emits kernels and loops.
 #include "krylov.cuh"
 #include <cmath>
+#include <cstdlib>
 
 namespace bbot {
 
@@ -280,9 +281,14 @@ void DevGmres::ensure(Dev& d, long long n_, int restart_) {
 
 void DevGmres::reset_total(Dev& d) { launch(d, k_gm_reset_total, dim3(1), dim3(1), 0, sc.p); }
 
+static int dot_parts_cap() {   // GPU-only tuning knob (env A/B): blocks of the CGS2 multi-dot kernels
+  static const int v = [] { const char* e = getenv("BBOT_DOT_PARTS"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
                     const double* scale, double tol, int maxit) {
-  const int parts = red.parts_for(n, 1);
+  const int parts = dot_parts_cap() > 0 ? std::min(red.parts_for(n, 1), dot_parts_cap()) : red.parts_for(n, 1);
   const unsigned nb = nblocks(n, BS);
   const unsigned nb_upd = std::min<unsigned>(nb, 8u * d.num_sms);
   GmresScal* G = sc.p;
