@@ -63,6 +63,11 @@ typedef struct {
   double omega_T;      /* l1-Jacobi weight, AMG(T) [1.0] (D = sum_j |T_ij|, I3)             */
   int coarse_max_A;    /* AMG(A) coarsest: max rows per time slice [64]                     */
   int coarse_max_T;    /* AMG(T) coarsest: max rows in total [1024]                         */
+  int precond;         /* 0 = BB on (4.17) [0]; 1 = SIMPLE on the saddle-point system
+                        * (eq:saddle-point) with eq:sca-precs: FGMRES
+                        * on J = [[A, B^T],[B, -C]], rhs (f; g~); the inner solve is
+                        * S-hat = C + B diag(A)^-1 B^T (stored in T's slot, A31/A32) by
+                        * GMRES(restart_T) + AMG, eps_T; recovery dphi = x1, drho = x2.   */
 } bbot_solver_opts;
 
 typedef struct {
@@ -92,6 +97,7 @@ typedef struct {
   int max_mu_steps;         /* [0 = all] truncate the mu schedule                           */
   double mu_tight;          /* [0.3]   below this mu the A_k solves tighten ... (A14')       */
   double eps_A_tight;       /* [1e-5]  ... to this relative tolerance                        */
+  double simple_below_mu;   /* [0]     A34: SIMPLE (precond 1) for every mu below this       */
 } bbot_ipm_opts;
 
 typedef struct {
@@ -150,14 +156,18 @@ bbot_status bbot_residual(bbot_ctx* ctx, double* F_phi, double* F_rho, double* F
 
 /* a1 + a3: per-Newton-step assembly at the current state: edge weights, grad phi,
  * C = Mbar diag(s/rho) (A7), RHS (f; P g~) ((4.17)), Atilde,
- * T = C Mbar^-1 Atilde - B M^-1 Btilde ((4.26), A8) and both AMG hierarchies. */
+ * T = C Mbar^-1 Atilde - B M^-1 Btilde ((4.26), A8) and both AMG hierarchies.
+ * With precond = 1 (SIMPLE): RHS (f; g~), S-hat in place of T, AMG(S-hat) only. */
 bbot_status bbot_assemble(bbot_ctx* ctx);
 
-/* a2: y = J_P x with J_P = [[A, B^T P^T],[P B, -P C P^T]] ((4.17)).
+/* a2: y = J_P x with J_P = [[A, B^T P^T],[P B, -P C P^T]] ((4.17));
+ * after a SIMPLE assembly, y = J x with J = [[A, B^T],[B, -C]].
  * x, y: n+m vectors. Requires bbot_assemble. */
 bbot_status bbot_jp_matvec(bbot_ctx* ctx, const double* x, double* y, bbot_mem mem);
 
-/* a4: z = BB-preconditioner applied to r (n+m): T z2 = -r2 (GMRES+AMG(T)),
+/* a4: z = BB-preconditioner applied to r (n+m) -- or, after a SIMPLE assembly, the
+ * SIMPLE preconditioner (eq:sca-precs; inner_T_its = S-hat GMRES its, A its 0):
+ * T z2 = -r2 (GMRES+AMG(T)),
  * y = P^T Mbar^-1 Atilde z2, b = r1 - B^T P^T y (slice means removed),
  * A_k x^k = b^k (PCG+AMG(A)), out (x; y)  ((4.18)-(4.20), (4.26), A9, A12, A14). */
 bbot_status bbot_bb_apply(bbot_ctx* ctx, const double* r, double* z, bbot_mem mem,
@@ -182,7 +192,7 @@ bbot_status bbot_ipm_run(bbot_ctx* ctx, const bbot_ipm_opts* o, bbot_ipm_stats* 
 bbot_status bbot_kinetic_energy(bbot_ctx* ctx, double* ke);
 
 /* ---- inspection (parity tests, profiling) ---- */
-/* T as host CSR (rows m; columns sorted).  Call with rowptr == NULL to get nnz. */
+/* T (or S-hat after a SIMPLE assembly) as host CSR (rows m; columns sorted).  Call with rowptr == NULL to get nnz. */
 bbot_status bbot_get_T(bbot_ctx* ctx, long long* nnz, long long* rowptr, int* cols, double* vals);
 /* which: 0 = AMG(A), 1 = AMG(T).  sizes: >= 32 entries. */
 bbot_status bbot_amg_info(bbot_ctx* ctx, int which, int* nlevels, long long* sizes);

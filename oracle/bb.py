@@ -38,6 +38,7 @@ class SolverOpts:
     coarse_max_A: int = 64        # rows per slice
     coarse_max_T: int = 1024      # rows in total
     exact_inner: bool = False     # pin mode: exact T solve + exact A_k^+ (no AMG)
+    precond: str = "bb"           # "bb" (§4.5) or "simple" (§5.3, NEXT row f1)
 
 
 class BBSolver:

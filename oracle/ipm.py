@@ -9,6 +9,8 @@ A18 at least one Newton step per mu, stop when ||F(x;mu)|| <= max(1e-2 mu, 1e-11
 eps_A (1e-3) to eps_A_tight (1e-5) once mu < mu_tight (0.3) -- the Newton systems'
 conditioning grows as mu -> 0 and the outer FGMRES needs a more accurate
 preconditioner (C2 at mu = 0.25: 400-cap at 1e-3, 74 iterations at 1e-5).
+A34: the mu-switched BB -> SIMPLE hybrid ("SIMPLE ... becomes
+faster in the last IP iterations"): SIMPLE (oracle/simple.py) once mu < simple_below_mu.
 """
 from __future__ import annotations
 
@@ -17,6 +19,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from .bb import BBSolver, SolverOpts
+from .simple import SimpleSolver
 from .ops import Discretisation
 
 
@@ -32,6 +35,7 @@ class IpmOpts:
     max_mu_steps: int | None = None     # truncate the schedule (tests)
     mu_tight: float = 0.3               # A14': below this mu the A_k solves tighten ...
     eps_A_tight: float = 1e-5           # ... to this relative tolerance
+    simple_below_mu: float = 0.0        # A34: SIMPLE instead of BB once mu < this (0 = never)
 
 
 def step_length(rho, s, drho, ds, tau):
@@ -57,7 +61,7 @@ def res_norm(d, phi, rho, s, mu):
 
 
 def newton_step(d: Discretisation, phi, rho, s, mu, opts: SolverOpts, tau: float):
-    S = BBSolver(d, phi, rho, s, mu, opts)
+    S = (SimpleSolver if opts.precond == "simple" else BBSolver)(d, phi, rho, s, mu, opts)
     dphi, drho, ds = S.solve()
     alpha = step_length(rho, s, drho, ds, tau)
     phi = phi + alpha * dphi
@@ -100,6 +104,8 @@ def ipm_run(d: Discretisation, phi, rho, s, ipm: IpmOpts | None = None,
         tol = max(ipm.newton_rel_tol * mu, ipm.newton_abs_floor) * F0
         for it in range(ipm.newton_max):
             o_mu = opts if mu >= ipm.mu_tight else replace(opts, eps_A=min(opts.eps_A, ipm.eps_A_tight))
+            if mu < ipm.simple_below_mu:
+                o_mu = replace(o_mu, precond="simple")
             phi, rho, s, alpha, st = newton_step(d, phi, rho, s, mu, o_mu, ipm.frac_to_boundary)
             r = res_norm(d, phi, rho, s, mu)
             rec = dict(mu=mu, newton=it, alpha=alpha, res=r, **st)

@@ -24,7 +24,8 @@ class SolverOpts(C.Structure):
     _fields_ = [("eps_out", C.c_double), ("eps_T", C.c_double), ("eps_A", C.c_double),
                 ("restart", C.c_int), ("maxit", C.c_int), ("restart_T", C.c_int),
                 ("maxit_inner", C.c_int), ("omega_A", C.c_double), ("omega_T", C.c_double),
-                ("coarse_max_A", C.c_int), ("coarse_max_T", C.c_int)]
+                ("coarse_max_A", C.c_int), ("coarse_max_T", C.c_int),
+                ("precond", C.c_int)]   # 0 = BB, 1 = SIMPLE (NEXT f1)
 
 
 class SolveStats(C.Structure):
@@ -42,7 +43,8 @@ class IpmOpts(C.Structure):
     _fields_ = [("mu0", C.c_double), ("mu_factor", C.c_double), ("mu_min", C.c_double),
                 ("newton_rel_tol", C.c_double), ("newton_abs_floor", C.c_double),
                 ("frac_to_boundary", C.c_double), ("newton_max", C.c_int), ("max_mu_steps", C.c_int),
-                ("mu_tight", C.c_double), ("eps_A_tight", C.c_double)]
+                ("mu_tight", C.c_double), ("eps_A_tight", C.c_double),
+                ("simple_below_mu", C.c_double)]   # A34 hybrid
 
 
 class IpmRecord(C.Structure):

@@ -86,7 +86,7 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
       fi_tbe((size_t)FI_MAX * TB_MAX * nbar, -1), fi_tbpL((size_t)FI_MAX * TB_MAX * nbar, 0),
       fi_tbpR((size_t)FI_MAX * TB_MAX * nbar, 0), ca_pos(3 * (size_t)nbar, 0);
   std::vector<double> fi_alpha((size_t)FI_MAX * FI_EMAX * nbar, 0.0), fi_tbbeta((size_t)FI_MAX * TB_MAX * nbar, 0.0);
-  std::vector<std::vector<int>> S(nbar);
+  std::vector<std::vector<int>> S(nbar), Fl(nbar);
   int W = 0;
   for (int i = 0; i < nbar; i++) {
     std::vector<int> F = {3 * i, 3 * i + 1, 3 * i + 2};
@@ -98,6 +98,7 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
     }
     for (int f : foreign) F.push_back(f);
     BB_REQUIRE((int)F.size() <= FI_MAX, BBOT_E_GEOMETRY, "B row too wide");
+    Fl[i] = F;
     std::set<int> cols;
     for (int f : F) {
       cols.insert(f / 3);
@@ -146,6 +147,32 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
     }
   }
   BB_REQUIRE(W <= W_MAX, BBOT_E_GEOMETRY, "T stencil wider than W_MAX");
+  // SIMPLE (NEXT f1): S-hat = C + B diag(A)^-1 B^T couples rows i, j whose B rows share a
+  // fine cell; every such j lies in S(i) (a fine cell adjacent to a child of j across a
+  // coarse boundary is reached through a type-b edge), so S-hat uses T's pattern.
+  {
+    std::vector<std::vector<std::pair<int, int>>> holders(N);   // f -> (j, index of f in F(j))
+    for (int j = 0; j < nbar; j++)
+      for (size_t q = 0; q < Fl[j].size(); q++) holders[Fl[j][q]].push_back({j, (int)q});
+    std::vector<int> fv_j((size_t)FI_MAX * FV_MAX * nbar, -1), fv_q((size_t)FI_MAX * FV_MAX * nbar, 0),
+        fv_pos((size_t)FI_MAX * FV_MAX * nbar, 0);
+    for (int i = 0; i < nbar; i++)
+      for (size_t q = 0; q < Fl[i].size(); q++) {
+        const auto& hl = holders[Fl[i][q]];
+        BB_REQUIRE((int)hl.size() <= FV_MAX, BBOT_E_GEOMETRY, "fine cell in too many B rows");
+        for (size_t t = 0; t < hl.size(); t++) {
+          auto it = std::find(S[i].begin(), S[i].end(), hl[t].first);
+          BB_REQUIRE(it != S[i].end(), BBOT_E_INTERNAL, "S-hat column outside the T pattern");
+          size_t at = (q * FV_MAX + t) * nbar + i;
+          fv_j[at] = hl[t].first;
+          fv_q[at] = hl[t].second;
+          fv_pos[at] = (int)(it - S[i].begin());
+        }
+      }
+    g.fv_j.upload(fv_j, s);
+    g.fv_q.upload(fv_q, s);
+    g.fv_pos.upload(fv_pos, s);
+  }
   g.W = W;
   long long ssum = 0;
   for (int i = 0; i < nbar; i++) ssum += (long long)S[i].size();
@@ -170,6 +197,8 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
   for (int k = 0; k < K; k++) std::fill(slT.begin() + (size_t)k * nbar, slT.begin() + (size_t)(k + 1) * nbar, k);
   g.slice_A.upload(slA, s);
   g.slice_T.upload(slT, s);
+  std::vector<int> slS((size_t)nbar * K, 0);
+  g.slice_S.upload(slS, s);
   BB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -361,8 +390,11 @@ void compute_residual(bbot_ctx* c, bool write_rhs) {
   if (write_rhs) {
     c->red.slice_sum(GtSum{g.nbar, A.gt.p}, g.nbar, K, sc + 2 * K + 1, false);
     BB_CUDA(cudaMemcpyAsync(A.rhs.p, A.f.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    launch(c->dev, k_rhs2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, g.area, (const double*)g.cbar.p,
-           (const double*)A.gt.p, (const double*)(sc + 2 * K + 1), A.rhs.p + n);
+    if (c->opts.precond == 1)    // SIMPLE: the unprojected saddle-point system
+      BB_CUDA(cudaMemcpyAsync(A.rhs.p + n, A.gt.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    else
+      launch(c->dev, k_rhs2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, g.area, (const double*)g.cbar.p,
+             (const double*)A.gt.p, (const double*)(sc + 2 * K + 1), A.rhs.p + n);
   }
   BB_CUDA(cudaMemcpyAsync(hs.data(), sc, (2 * K + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
   sync(c->dev);
@@ -436,11 +468,91 @@ __global__ void __launch_bounds__(128) k_assemble_T(
   }
 }
 
+// ---------------------------------------------------------------- S-hat assembly (NEXT f1)
+// SIMPLE (A31): S-hat = -S~ = C + B diag(A)^-1 B^T, block tridiagonal,
+// in T's slice-shared ELL layout.  Row (k0, i):
+//   sum over phi slices kp in {k0, k0+1}, fine cells f in F(i), rows (k1, j) of B holding f:
+//   B[(k0,i),(kp,f)] / A_kp[f,f] * B[(k1,j),(kp,f)],   k1 in {kp (side 0), kp-1 (side 1)}
+// plus C[(k0,i)] on the diagonal.  B entries as in k_assemble_T / BRow (D5, A5).
+__global__ void k_dainv(long long n, int N, const double* __restrict__ Aoff, double* __restrict__ dAinv) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int kk = (int)(r / N);
+  int f = (int)(r - (long long)kk * N);
+  const double* o = Aoff + (size_t)kk * 4 * N + f;
+  double d = 0.0;
+#pragma unroll
+  for (int t = 0; t < 4; t++) d -= o[(size_t)t * N];     // pad slots hold 0
+  dAinv[r] = 1.0 / d;
+}
+
+__global__ void __launch_bounds__(128) k_assemble_S(
+    int nbar, int K, int N, int NE, int W, double dt, const double* __restrict__ cf,
+    const double* __restrict__ gphi, const double* __restrict__ dAinv, const double* __restrict__ Cd,
+    const int* __restrict__ fi_cell, const int* __restrict__ fi_child, const int* __restrict__ fi_edge,
+    const double* __restrict__ fi_alpha, const int* __restrict__ fv_j, const int* __restrict__ fv_q,
+    const int* __restrict__ fv_pos, double* __restrict__ Sv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbar) return;
+  int kb = blockIdx.y * T_KCH, ke = min(K, kb + T_KCH);
+  for (int k0 = kb; k0 < ke; k0++) {
+    double acc[3 * W_MAX];
+    for (int t = 0; t < 3 * W; t++) acc[t] = 0.0;
+    for (int side = 0; side < 2; side++) {
+      int kp = k0 + side;
+      const double* gk = gphi + (size_t)kp * NE;
+      const double* dinv = dAinv + (size_t)kp * N;
+      for (int q = 0; q < FI_MAX; q++) {
+        int f = fi_cell[q * nbar + i];
+        if (f < 0) break;
+        double tp = fi_child[q * nbar + i] ? cf[f] / dt : 0.0;
+        double sp = 0.0;
+        for (int e = 0; e < FI_EMAX; e++) {
+          int ed = fi_edge[(q * FI_EMAX + e) * nbar + i];
+          if (ed < 0) break;
+          sp += fi_alpha[(q * FI_EMAX + e) * nbar + i] * gk[ed];
+        }
+        double w = ((side ? tp : -tp) + sp) * dinv[f];
+        for (int t = 0; t < FV_MAX; t++) {
+          size_t at = (size_t)(q * FV_MAX + t) * nbar + i;
+          int j = fv_j[at];
+          if (j < 0) break;
+          int qj = fv_q[at], pj = fv_pos[at];
+          double tpj = fi_child[qj * nbar + j] ? cf[f] / dt : 0.0;
+          double spj = 0.0;
+          for (int e = 0; e < FI_EMAX; e++) {
+            int ed = fi_edge[(qj * FI_EMAX + e) * nbar + j];
+            if (ed < 0) break;
+            spj += fi_alpha[(qj * FI_EMAX + e) * nbar + j] * gk[ed];
+          }
+          if (kp <= K - 1) acc[(kp - k0 + 1) * W + pj] += w * (spj - tpj);   // row (kp, j), side 0
+          if (kp >= 1) acc[(kp - k0) * W + pj] += w * (spj + tpj);           // row (kp-1, j), side 1
+        }
+      }
+    }
+    acc[W] += Cd[(size_t)k0 * nbar + i];
+    for (int d = 0; d < 3; d++)
+      for (int sl = 0; sl < W; sl++) Sv[((size_t)(k0 * 3 + d) * W + sl) * nbar + i] = acc[d * W + sl];
+  }
+}
+
 void assemble_T(bbot_ctx* c) {
   DevGeom& g = c->g;
   Assembled& A = c->as;
   size_t nv = (size_t)g.K * 3 * g.W * g.nbar;
   if (A.Tv.n != nv) A.Tv.alloc(nv, c->dev.stream);
+  A.precond = c->opts.precond;
+  if (c->opts.precond == 1) {
+    if (A.dAinv.n != (size_t)c->n()) A.dAinv.alloc(c->n(), c->dev.stream);
+    launch(c->dev, k_dainv, dim3(nblocks(c->n(), 256)), dim3(256), 0, c->n(), g.N, (const double*)A.Aoff.p,
+           A.dAinv.p);
+    dim3 grid(nblocks(g.nbar, 128), (g.K + T_KCH - 1) / T_KCH);
+    launch(c->dev, k_assemble_S, grid, dim3(128), 0, g.nbar, g.K, g.N, g.NE, g.W, g.dt, (const double*)g.c.p,
+           (const double*)A.gphi.p, (const double*)A.dAinv.p, (const double*)A.Cd.p, (const int*)g.fi_cell.p,
+           (const int*)g.fi_child.p, (const int*)g.fi_edge.p, (const double*)g.fi_alpha.p, (const int*)g.fv_j.p,
+           (const int*)g.fv_q.p, (const int*)g.fv_pos.p, A.Tv.p);
+    return;
+  }
   dim3 grid(nblocks(g.nbar, 128), (g.K + T_KCH - 1) / T_KCH);
   launch(c->dev, k_assemble_T, grid, dim3(128), 0, g.nbar, g.K, g.NE, g.NEbar, g.W, g.dt, (const double*)g.c.p,
          (const double*)A.gphi.p, (const double*)A.omegabar.p, (const double*)A.sr.p, (const int*)g.cadj_e.p,

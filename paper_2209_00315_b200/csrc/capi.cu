@@ -48,6 +48,7 @@ void check_opts(const bbot_solver_opts& o) {
   BB_REQUIRE(o.omega_A > 0 && o.omega_A < 2 && o.omega_T > 0 && o.omega_T < 2, BBOT_E_INPUT, "bad Jacobi weight");
   BB_REQUIRE(o.coarse_max_A >= 2 && o.coarse_max_A <= 120 && o.coarse_max_T >= 1 && o.coarse_max_T <= 8192,
              BBOT_E_INPUT, "bad coarse sizes");
+  BB_REQUIRE(o.precond == 0 || o.precond == 1, BBOT_E_INPUT, "precond must be 0 (BB) or 1 (SIMPLE)");
 }
 
 }  // namespace
@@ -67,6 +68,7 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->omega_T = 1.0;
   o->coarse_max_A = 64;
   o->coarse_max_T = 1024;
+  o->precond = 0;
 }
 
 void bbot_default_ipm_opts(bbot_ipm_opts* o) {
@@ -81,6 +83,7 @@ void bbot_default_ipm_opts(bbot_ipm_opts* o) {
   o->max_mu_steps = 0;
   o->mu_tight = 0.3;
   o->eps_A_tight = 1e-5;
+  o->simple_below_mu = 0.0;
 }
 
 bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt, int K, const double* rho_in,
@@ -263,7 +266,8 @@ bbot_status bbot_jp_matvec(bbot_ctx* c, const double* x, double* y, bbot_mem mem
   long long nm = c->n() + c->m();
   if (c->tmp_nm.n != (size_t)nm) { c->tmp_nm.alloc(nm, c->dev.stream); c->tmp_nm2.alloc(nm, c->dev.stream); }
   copy_in(c, c->tmp_nm.p, x, nm, mem);
-  jp_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);
+  if (c->as.precond == 1) j_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);   // SIMPLE: (eq:saddle-point)
+  else jp_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);
   copy_out(c, y, c->tmp_nm2.p, nm, mem);
   sync(c->dev);
   API_END(c)
@@ -328,11 +332,17 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
   if (o.max_mu_steps > 0 && (int)mus.size() > o.max_mu_steps) mus.resize(o.max_mu_steps);
   BB_REQUIRE(o.eps_A_tight > 0, BBOT_E_INPUT, "bad eps_A_tight");
   const double eps_A0 = c->opts.eps_A;
-  struct Restore {           // the caller's eps_A comes back even if a solve throws
+  const int precond0 = c->opts.precond;
+  struct Restore {           // the caller's eps_A and preconditioner come back even if a solve throws
     double& ref;
     double val;
-    ~Restore() { ref = val; }
-  } restore{c->opts.eps_A, eps_A0};
+    int& pref;
+    int pval;
+    ~Restore() {
+      ref = val;
+      pref = pval;
+    }
+  } restore{c->opts.eps_A, eps_A0, c->opts.precond, precond0};
   c->mu = o.mu0;
   compute_residual(c, false);
   double F0 = c->as.res_norm;
@@ -340,6 +350,8 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
     c->mu = mu;
     // A14': tighter A_k solves once mu < mu_tight (the solve graph is re-captured per assembly)
     c->opts.eps_A = mu >= o.mu_tight ? eps_A0 : std::min(eps_A0, o.eps_A_tight);
+    // A34: the mu-switched BB -> SIMPLE hybrid
+    if (mu < o.simple_below_mu) c->opts.precond = 1;
     double tol = std::max(o.newton_rel_tol * mu, o.newton_abs_floor) * F0;   // A18
     for (int it = 0; it < o.newton_max; it++) {
       bbot_ipm_record rec;
@@ -361,6 +373,7 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
     }
   }
   c->opts.eps_A = eps_A0;
+  c->opts.precond = precond0;
   S.final_mu = c->mu;
   S.kinetic_energy = kinetic_energy(c);
   S.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -22,6 +22,7 @@ constexpr int FI_MAX = 9;    // fine cells in a B row (3 children + <= 6 across 
 constexpr int FI_EMAX = 4;   // edges of E(i) incident to such a fine cell
 constexpr int TB_MAX = 2;    // type-b edges of a fine cell
 constexpr int W_MAX = 16;    // T spatial stencil width cap
+constexpr int FV_MAX = 6;    // coarse cells j whose B row holds a given fine cell (SIMPLE)
 
 struct DevGeom {
   int nbar = 0, N = 0, NE = 0, NEbar = 0, K = 0, W = 0;
@@ -48,7 +49,11 @@ struct DevGeom {
   DBuf<double> fi_tbbeta;                     // [FI_MAX][TB_MAX][nbar] 1/2 R_f[sigma,f]|e|
   DBuf<int> fi_tbpL, fi_tbpR;                 // [FI_MAX][TB_MAX][nbar] pos of par L/R in S(i)
   DBuf<int> ca_pos;                           // [3][nbar] pos of coarse neighbour in S(i)
+  // SIMPLE S-hat assembly (NEXT f1): for the q-th fine cell f of B row i, the rows j whose
+  // B row also holds f: j, the index of f in F(j), and the position of j in S(i)
+  DBuf<int> fv_j, fv_q, fv_pos;               // [FI_MAX][FV_MAX][nbar], fv_j = -1 pad
   DBuf<int> slice_A, slice_T;                 // row -> slice for AMG level 0
+  DBuf<int> slice_S;                          // all 0: AMG(S-hat) aggregates across time (A32)
 };
 
 struct Assembled {
@@ -58,8 +63,10 @@ struct Assembled {
   DBuf<double> omegabar;          // [K][NEbar]
   DBuf<double> Cd, sr;            // C = cbar s/rho, s/rho  (m)
   DBuf<double> f, g, h, gt;       // RHS pieces
-  DBuf<double> rhs;               // (f; P gt)  (n+m)
-  DBuf<double> Tv;                // [K][3][W][nbar]
+  DBuf<double> rhs;               // (f; P gt) (BB) or (f; gt) (SIMPLE)  (n+m)
+  DBuf<double> Tv;                // [K][3][W][nbar]: T (BB) or S-hat = C + B diag(A)^-1 B^T (SIMPLE)
+  DBuf<double> dAinv;             // 1 / diag(A)  (n; SIMPLE)
+  int precond = 0;                // preconditioner the assembly was built for
   double scale = 0;               // ||(f;g;h)||
   DBuf<double> dscale;            // the same on the device (read by the captured solve)
   double res_norm = 0;            // ||F||

@@ -163,6 +163,64 @@ void jp_matvec(bbot_ctx* c, const double* x, double* y) {
          (const double*)g.cbar.p, (const double*)S2, 1.0 / g.area);
 }
 
+// ---------------------------------------------------------------- NEXT f1: SIMPLE
+// J on the saddle-point system (eq:saddle-point): y1 = A x1 + B^T x2, y2 = B x1 - C x2
+__global__ void k_j_y2(long long m, int nbar, BRow br, const double* __restrict__ x1, const double* __restrict__ x2,
+                       const double* __restrict__ Cd, double* __restrict__ y2) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  y2[t] = br(x1, k0, t - (long long)k0 * nbar) - Cd[t] * x2[t];
+}
+
+void j_matvec(bbot_ctx* c, const double* x, double* y) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)c->as.Aoff.p,
+         (const int*)g.fadj_nb.p, make_btrow(c), x, x + n, (const double*)nullptr, 0.0, y);
+  launch(c->dev, k_j_y2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, make_brow(c), x, x + n,
+         (const double*)c->as.Cd.p, y + n);
+}
+
+// SIMPLE apply (eq:sca-precs), step 1: z1 = diag(A)^-1 r1 (into w), c = r2 - B z1 (into cvec)
+__global__ void k_simple_z1(long long n, const double* __restrict__ r1, const double* __restrict__ dAinv,
+                            double* __restrict__ z1) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) z1[t] = r1[t] * dAinv[t];
+}
+__global__ void k_simple_c(long long m, int nbar, BRow br, const double* __restrict__ r2,
+                           const double* __restrict__ z1, double* __restrict__ cvec) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  cvec[t] = r2[t] - br(z1, k0, t - (long long)k0 * nbar);
+}
+// step 3: out1 = diag(A)^-1 (r1 - B^T z2), out2 = z2
+__global__ void k_simple_out(long long n, long long m, int N, BtRow bt, const double* __restrict__ r1,
+                             const double* __restrict__ dAinv, const double* __restrict__ z2,
+                             double* __restrict__ out) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    int kk = (int)(t / N);
+    out[t] = (r1[t] - bt(z2, nullptr, 0.0, kk, t - (long long)kk * N)) * dAinv[t];
+  } else if (t < n + m) {
+    out[t] = z2[t - n];
+  }
+}
+
+void simple_c(bbot_ctx* c, const double* r, double* z1, double* cvec) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_simple_z1, dim3(nblocks(n, BS)), dim3(BS), 0, n, r, (const double*)c->as.dAinv.p, z1);
+  launch(c->dev, k_simple_c, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, make_brow(c), r + n, (const double*)z1,
+         cvec);
+}
+void simple_out(bbot_ctx* c, const double* r, const double* z2, double* out) {
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_simple_out, dim3(nblocks(n + m, BS)), dim3(BS), 0, n, m, c->g.N, make_btrow(c), r,
+         (const double*)c->as.dAinv.p, z2, out);
+}
+
 // ---------------------------------------------------------------- y = T x, y = A x
 template <class V>
 __global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y) {
@@ -272,6 +330,13 @@ void recover(bbot_ctx* c) {
   long long n = c->n(), m = c->m();
   int K = g.K;
   cudaStream_t s = c->dev.stream;
+  if (c->as.precond == 1) {    // SIMPLE on (eq:saddle-point): dphi = x1, drho = x2, ds
+    BB_CUDA(cudaMemcpyAsync(c->dphi.p, c->sol.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    BB_CUDA(cudaMemcpyAsync(c->drho.p, c->sol.p + n, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    launch(c->dev, k_ds, dim3(nblocks(m, BS)), dim3(BS), 0, m, (const double*)c->as.h.p, (const double*)c->s.p,
+           (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p);
+    return;
+  }
   double* S = c->scal.p;
   double* shift = c->scal.p + 2 * (K + 2);
   // drho = P^T y  (A30)

@@ -19,6 +19,9 @@ void apply_T(bbot_ctx* c, const double* x, double* y);                      // y
 void bb_y_from_z(bbot_ctx* c, const double* z, double* y);                  // y = P^T Mbar^-1 Atilde z
 void bb_rhs_A(bbot_ctx* c, const double* r1, const double* y, double* b);   // b = r1 - B^T y, slice means removed
 void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L);         // arithmetic mean per slice
+void j_matvec(bbot_ctx* c, const double* x, double* y);                     // (eq:saddle-point)
+void simple_c(bbot_ctx* c, const double* r, double* z1, double* cvec);      // z1 = diag(A)^-1 r1, c = r2 - B z1
+void simple_out(bbot_ctx* c, const double* r, const double* z2, double* out);  // (diag(A)^-1(r1 - B^T z2); z2)
 void recover(bbot_ctx* c);                                                   // a6
 double newton_update(bbot_ctx* c, double tau);                              // a7 step + renormalise
 double kinetic_energy(bbot_ctx* c);

@@ -53,7 +53,10 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   double ta = t0.ms();
   EvTimer t1(c->dev.stream);
   AmgWork& w = c->amgw;
-  if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
+  if (c->as.precond == 1) {   // SIMPLE: one hierarchy, on S-hat (the A block is inverted by its diagonal)
+    c->amgA.clear();
+    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_T, w);
+  } else if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
     amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
     amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
   } else {
@@ -152,14 +155,40 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
 }
 
+// NEXT f1: z = SIMPLE(r) (eq:sca-precs; oracle/simple.py):
+//   z1 = diag(A)^-1 r1;  S-hat z2 = B z1 - r2 by GMRES(restart_T) + one AMG(S-hat) V-cycle,
+//   relative eps_T (A32);  out = (diag(A)^-1 (r1 - B^T z2); z2)
+static void emit_simple_apply(bbot_ctx* c, const double* r, double* z) {
+  const bbot_solver_opts& o = c->opts;
+  long long m = c->m();
+  simple_c(c, r, c->tmp_n2.p, c->tmp_m2.p);
+  dev_neg_norm(c->dev, c->red, c->tmp_m2.p, c->tmp_m.p, m, c->nrm_T.p);
+  SliceEllView vS = view_T(c);
+  c->innerT.emit(
+      c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
+      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgT, vS, x, y); }, c->tmp_m.p, c->tmp_m2.p,
+      c->nrm_T.p, o.eps_T, o.maxit_inner);
+  simple_out(c, r, c->tmp_m2.p, z);
+}
+
+static void emit_apply(bbot_ctx* c, const double* r, double* z) {
+  if (c->as.precond == 1) emit_simple_apply(c, r, z);
+  else emit_bb_apply(c, r, z);
+}
+
 // a5 + a6
 static void emit_solve(bbot_ctx* c) {
   const bbot_solver_opts& o = c->opts;
   c->innerT.reset_total(c->dev);
   c->pcg.reset_stats(c->dev);
+  const bool simple = c->as.precond == 1;
   c->outer.emit(
-      c->dev, c->red, [&](const double* x, double* y) { jp_matvec(c, x, y); },
-      [&](const double* x, double* y) { emit_bb_apply(c, x, y); }, c->as.rhs.p, c->sol.p, c->as.dscale.p,
+      c->dev, c->red,
+      [&](const double* x, double* y) {
+        if (simple) j_matvec(c, x, y);
+        else jp_matvec(c, x, y);
+      },
+      [&](const double* x, double* y) { emit_apply(c, x, y); }, c->as.rhs.p, c->sol.p, c->as.dscale.p,
       o.eps_out, o.maxit);
   recover(c);
 }
@@ -211,7 +240,7 @@ void bb_apply(bbot_ctx* c, const double* r, double* z, int* its_T, int* its_A_ma
   prepare(c);
   c->innerT.reset_total(c->dev);
   c->pcg.reset_stats(c->dev);
-  emit_bb_apply(c, r, z);
+  emit_apply(c, r, z);
   GmresScal gT;
   PcgScal pA;
   BB_CUDA(cudaMemcpyAsync(&gT, c->innerT.sc.p, sizeof(gT), cudaMemcpyDeviceToHost, c->dev.stream));

@@ -39,6 +39,7 @@ def test_oracle_defaults_agree_with_library():
     for f in ("eps_out", "eps_T", "eps_A", "restart", "maxit", "restart_T", "maxit_inner",
               "omega_A", "omega_T", "coarse_max_A", "coarse_max_T"):
         assert getattr(o, f) == getattr(s, f), f
+    assert o.precond == 0 and s.precond == "bb"
 
 
 def test_oracle_ipm_defaults_agree_with_library():
@@ -47,7 +48,7 @@ def test_oracle_ipm_defaults_agree_with_library():
     from oracle.ipm import IpmOpts
     o, s = pb.default_ipm_opts(), IpmOpts()
     for f in ("mu0", "mu_factor", "mu_min", "newton_rel_tol", "newton_abs_floor", "frac_to_boundary", "newton_max",
-              "mu_tight", "eps_A_tight"):
+              "mu_tight", "eps_A_tight", "simple_below_mu"):
         assert getattr(o, f) == getattr(s, f), f
 
 

@@ -1,0 +1,121 @@
+"""GPU parity of NEXT row f1 -- the SIMPLE preconditioner on the
+saddle-point system (eq:saddle-point) -- against oracle/simple.py.
+Tolerances as tests/test_gpu_parity.py."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+from oracle.bb import SolverOpts                      # noqa: E402
+from oracle.ops import Discretisation                 # noqa: E402
+from oracle.simple import S_hat, SimpleSolver         # noqa: E402
+from synthetic import initial_state, make_problem, random_state   # noqa: E402
+
+
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2209_00315_b200 as pb
+    return pb
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def _ctx(name, state="random", mu=1e-2, seed=3, eps_out=1e-10):
+    pb = _gpu()
+    p = make_problem(name)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=seed, mu=mu) if state == "random" else initial_state(p, mu)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, opts=pb.default_solver_opts(precond=1, eps_out=eps_out))
+    ctx.set_state(phi, rho, s, mu)
+    return pb, p, d, ctx, (phi, rho, s, mu)
+
+
+@pytest.mark.parametrize("name", ["T1", "C1", "T2b"])
+def test_S_hat_and_J_parity(name):
+    """Ŝ = C + B diag(A)^{-1} B^T entrywise (A31) and J x (eq:saddle-point)."""
+    pb, p, d, ctx, (phi, rho, s, mu) = _ctx(name)
+    ctx.assemble()
+    rp, ci, cv = ctx.get_T()
+    Sg = sp.csr_matrix((cv, ci, rp), shape=(d.m, d.m))
+    So = S_hat(d, phi, rho, s)
+    assert abs(Sg - So).max() <= 1e-12 * abs(So).max()
+    S = SimpleSolver(d, phi, rho, s, mu, SolverOpts(precond="simple"))
+    x = np.random.default_rng(11).standard_normal(d.n + d.m)
+    assert _rel(ctx.jp_matvec(x), S.matvec(x)) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["T1", "C1"])
+def test_simple_amg_and_apply_parity(name):
+    """AMG(Ŝ) aggregates identical; one SIMPLE apply (eq:sca-precs) to 1e-8, same inner count."""
+    pb, p, d, ctx, (phi, rho, s, mu) = _ctx(name)
+    ctx.assemble()
+    S = SimpleSolver(d, phi, rho, s, mu, SolverOpts(precond="simple"))
+    sizes = ctx.amg_info(1)
+    assert sizes == S.amgS.sizes
+    for lvl in range(len(sizes) - 1):
+        assert np.array_equal(ctx.amg_agg(1, lvl), S.amgS.levels[lvl].agg), lvl
+    r = np.random.default_rng(9).standard_normal(d.n + d.m)
+    zg, itS, itA = ctx.bb_apply(r)
+    zo = S.apply(r)
+    assert itS == S.inner_its and itA == 0
+    assert _rel(zg, zo) < 1e-8
+
+
+# SIMPLE needs many more outer iterations than BB and more with every refinement (P:1103-1110,
+# Table sol11: ~45 / 100 / 230 / 480 at mu = 1 for eps_out = 1e-5); the cases use the paper's
+# looser outer tolerances where 400 iterations do not reach 1e-10
+@pytest.mark.parametrize("name,state,mu,eps", [("T1", "random", 0.01, 1e-10), ("T2", "init", 1.0, 1e-8),
+                                               ("C1", "init", 1.0, 1e-4), ("C1", "random", 0.05, 1e-2)])
+def test_simple_direction_parity(name, state, mu, eps):
+    """Newton direction through SIMPLE-FGMRES + δs elimination: relative 1e-8 per block,
+    outer counts +-1."""
+    pb, p, d, ctx, (phi, rho, s, mu) = _ctx(name, state=state, mu=mu, eps_out=eps)
+    ctx.assemble()
+    dphi, drho, ds, st = ctx.solve()
+    S = SimpleSolver(d, phi, rho, s, mu, SolverOpts(precond="simple", eps_out=eps))
+    ophi, orho, os_ = S.solve()
+    assert S.stats["converged"] and st["converged"] == 1, (st, S.stats)
+    assert abs(st["outer_its"] - S.stats["outer_its"]) <= 1, (st, S.stats)
+    for a, b in ((dphi, ophi), (drho, orho), (ds, os_)):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_graph_and_eager_simple_identical():
+    pb, p, d, ctx, (phi, rho, s, mu) = _ctx("C1", mu=0.05)
+    out = []
+    for graph in (True, False):
+        ctx.set_exec_mode(graph)
+        ctx.set_state(phi, rho, s, mu)
+        ctx.assemble()
+        out.append(ctx.solve())
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
+    assert out[0][3]["outer_its"] == out[1][3]["outer_its"]
+
+
+def test_ipm_hybrid_T2():
+    """A34: full IPM on T2 with SIMPLE below mu = 2^-10 (BB above), oracle run live:
+    the same number of Newton systems, outer counts +-1 where both converged, final
+    kinetic energy to 1e-6 (north star)."""
+    from threadpoolctl import threadpool_limits
+    from oracle.ipm import IpmOpts, ipm_run
+    pb = _gpu()
+    p = make_problem("T2")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    thr = 2.0 ** -10 * 1.5
+    with threadpool_limits(1):
+        res = ipm_run(d, phi, rho, s, IpmOpts(simple_below_mu=thr), SolverOpts())
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts(simple_below_mu=thr))
+    assert st["n_systems"] == len(res.log)
+    for g, o in zip(log, res.log):
+        if g["converged"] and o["converged"]:
+            assert abs(g["outer_its"] - o["outer_its"]) <= 1, (g, o)
+    assert abs(st["kinetic_energy"] - res.kinetic_energy) <= 1e-6 * res.kinetic_energy
