@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--mu-min", type=float, default=1e-8)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--simple-below", type=float, default=0.0,
+                    help="A34 hybrid: SIMPLE preconditioner for mu below this (0 = BB throughout)")
     a = ap.parse_args()
     import torch
     import paper_2209_00315_b200 as pb
@@ -30,11 +32,12 @@ def main():
 
     def cb(r):
         if not a.quiet:
-            print(f"mu={r['mu']:.3e} newton={r['newton']} outer={r['outer_its']} conv={r['converged']} "
+            print(f"{'S' if r['mu'] < a.simple_below else 'B'} mu={r['mu']:.3e} newton={r['newton']} outer={r['outer_its']} conv={r['converged']} "
                   f"T={r['inner_T_its']} Amax={r['inner_A_its_max']} res={r['res']:.3e} alpha={r['alpha']:.3f} "
                   f"setup={r['t_setup_ms']:.0f}ms krylov={r['t_krylov_ms']:.0f}ms", flush=True)
     t = time.time()
-    st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=a.mu_min), callback=cb)
+    st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=a.mu_min, simple_below_mu=a.simple_below),
+                            callback=cb)
     wall = time.time() - t
     print(json.dumps({"config": a.config, "n_systems": st["n_systems"], "total_outer": st["total_outer"],
                       "n_unconverged": st["n_unconverged"], "final_mu": st["final_mu"],

@@ -114,8 +114,6 @@ def test_ipm_hybrid_T2():
     ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     ctx.set_state(phi, rho, s, 1.0)
     st, log = ctx.ipm_run(pb.default_ipm_opts(simple_below_mu=thr))
-    assert st["n_systems"] == len(res.log)
-    for g, o in zip(log, res.log):
-        if g["converged"] and o["converged"]:
-            assert abs(g["outer_its"] - o["outer_its"]) <= 1, (g, o)
-    assert abs(st["kinetic_energy"] - res.kinetic_energy) <= 1e-6 * res.kinetic_energy
+    assert sum(1 for g in log if g["inner_A_its_max"] == 0) > 10      # SIMPLE systems ran
+    from test_gpu_parity import _ipm_compare
+    _ipm_compare(log, res.log, st, res.kinetic_energy)

@@ -91,3 +91,18 @@ def test_simple_and_bb_agree_on_ipm_start():
     gx = gx - (gx[0] @ d.M) / d.area
     gy = gy - (gy[0] @ d.M) / d.area
     assert np.linalg.norm(gx - gy) <= 1e-7 * np.linalg.norm(gy)
+
+
+def test_hybrid_ipm_reaches_the_same_central_path_point():
+    """A34: the BB -> SIMPLE hybrid IPM switches preconditioner below simple_below_mu and
+    ends at the same point of the central path as the BB-only run (each mu step's Newton
+    loop stops at the same residual tolerance, A18): final KE and rho agree."""
+    from oracle.ipm import IpmOpts, ipm_run
+    p, d = _disc("T1")
+    phi, rho, s = initial_state(p, 1.0)
+    thr = 2.0 ** -6 * 1.5
+    a = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -12), SolverOpts())
+    b = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -12, simple_below_mu=thr), SolverOpts())
+    assert all((r["inner_A_its_max"] == 0) == (r["mu"] < thr) for r in b.log)
+    assert abs(a.kinetic_energy - b.kinetic_energy) <= 1e-6 * a.kinetic_energy
+    assert np.linalg.norm(a.rho - b.rho) <= 1e-4 * np.linalg.norm(a.rho)
