@@ -64,6 +64,9 @@ CONFIGS = {
     "T1": dict(L=1, K=4, dens=("gauss", (0.3, 0.3), (0.7, 0.7), 0.1, 1e-3), protocol="unit"),
     "T2": dict(L=2, K=8, dens=("gauss", (0.3, 0.3), (0.7, 0.7), 0.1, 1e-3), protocol="unit"),
     "T2b": dict(L=2, K=8, dens=("bump", (0.3, 0.3), (0.7, 0.7), 0.2), protocol="unit"),
+    # test case 3, compression: not a BASELINE config
+    "T2c": dict(L=2, K=8, dens=("compress", (0.5, 0.5), 0.35, 0.5), protocol="unit"),
+    "C1c": dict(L=3, K=8, dens=("compress", (0.5, 0.5), 0.35, 0.5), protocol="compression workload"),
     # BASELINE.json configs[0..4]
     "C1": dict(L=3, K=8, dens=("gauss", (0.3, 0.3), (0.7, 0.7), 0.1, 1e-3),
                protocol="full IPM, mu 1 -> 1e-8 by 0.5"),
@@ -94,6 +97,13 @@ def make_problem(name: str, L: int | None = None, K: int | None = None) -> Probl
     elif d[0] == "bump":
         _, c0, c1, radius = d
         fin, ffi = cos2_bump(*c0, radius), cos2_bump(*c1, radius)
+    elif d[0] == "compress":
+        # test case 3 (NEXT f3): a cos^2 bump compressed about its centre by the
+        # dilation x -> c + theta (x - c); the target theta^-2 b(|x - c| / theta) is the same
+        # bump with radius theta * r0 (unit mass after normalisation)
+        _, c, radius, theta = d
+        fin, ffi = cos2_bump(*c, radius), cos2_bump(*c, theta * radius)
+        info["compression"] = dict(centre=c, radius=radius, theta=theta)
     elif d[0] == "mix":
         fin, din = _random_mixture(d[1], 3, sigma_range=(0.05, 0.15), floor=1e-4)
         ffi, dfi = _random_mixture(d[2], 3, sigma_range=(0.05, 0.15), floor=1e-4)

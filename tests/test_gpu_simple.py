@@ -117,3 +117,22 @@ def test_ipm_hybrid_T2():
     assert sum(1 for g in log if g["inner_A_its_max"] == 0) > 10      # SIMPLE systems ran
     from test_gpu_parity import _ipm_compare
     _ipm_compare(log, res.log, st, res.kinetic_energy)
+
+
+def test_ipm_parity_compression_T2c():
+    """Test case 3, compression (NEXT f3), the BB stress case (the
+    Hessian term of Prop. 4.1 is non-zero): IPM mu 1 -> 2^-10 with BB, oracle run live,
+    trajectory parity and final KE to 1e-6."""
+    from threadpoolctl import threadpool_limits
+    from oracle.ipm import IpmOpts, ipm_run
+    from test_gpu_parity import _ipm_compare
+    pb = _gpu()
+    p = make_problem("T2c")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    with threadpool_limits(1):
+        res = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -10), SolverOpts())
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=2.0 ** -10))
+    _ipm_compare(log, res.log, st, res.kinetic_energy)
