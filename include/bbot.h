@@ -115,6 +115,9 @@ typedef struct {
   double final_mu;
   double kinetic_energy;    /* D12 at the final state                                       */
   double wall_ms;
+  int n_simple_fallback;    /* SIMPLE systems solved with BB instead: AMG(S-hat) could not be
+                             * built (a cross-slice coarse row wider than the Galerkin
+                             * capacity, BBOT_E_INTERNAL; A34)                            */
 } bbot_ipm_stats;
 
 void bbot_default_solver_opts(bbot_solver_opts* o);

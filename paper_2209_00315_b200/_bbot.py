@@ -55,7 +55,7 @@ class IpmRecord(C.Structure):
 class IpmStats(C.Structure):
     _fields_ = [("n_systems", C.c_int), ("total_outer", C.c_longlong), ("total_inner_T", C.c_longlong),
                 ("n_unconverged", C.c_int), ("final_mu", C.c_double), ("kinetic_energy", C.c_double),
-                ("wall_ms", C.c_double)]
+                ("wall_ms", C.c_double), ("n_simple_fallback", C.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -350,13 +350,22 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
     c->mu = mu;
     // A14': tighter A_k solves once mu < mu_tight (the solve graph is re-captured per assembly)
     c->opts.eps_A = mu >= o.mu_tight ? eps_A0 : std::min(eps_A0, o.eps_A_tight);
-    // A34: the mu-switched BB -> SIMPLE hybrid
-    if (mu < o.simple_below_mu) c->opts.precond = 1;
     double tol = std::max(o.newton_rel_tol * mu, o.newton_abs_floor) * F0;   // A18
     for (int it = 0; it < o.newton_max; it++) {
       bbot_ipm_record rec;
       memset(&rec, 0, sizeof(rec));
-      assemble_all(c, nullptr);
+      // A34: the mu-switched BB -> SIMPLE hybrid
+      c->opts.precond = mu < o.simple_below_mu ? 1 : precond0;
+      try {
+        assemble_all(c, nullptr);
+      } catch (const Error& e) {
+        // A34: AMG(S-hat) aggregates across time slices and can exceed the Galerkin row
+        // capacity on strongly anisotropic late-IPM states; that system is solved with BB
+        if (c->opts.precond != 1 || e.status != BBOT_E_INTERNAL) throw;
+        c->opts.precond = 0;
+        assemble_all(c, nullptr);
+        S.n_simple_fallback++;
+      }
       solve(c, &rec.solve);
       rec.alpha = newton_update(c, o.frac_to_boundary);
       c->have_dir = false;
