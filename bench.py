@@ -240,14 +240,16 @@ def roofline_of(ctx, prof_table, config):
     return roof, ranked, total_ms, models
 
 
-def scale_point(pb, config, dev, stream, steps=2):
+def scale_point(pb, config, dev, stream, steps=2, precond=0):
     """The same step on the largest single-GPU config (C4: 67.5 M unknowns, vectors of
-    0.4-0.5 GB, HBM-bound) -- reported beside the headline line, not instead of it."""
+    0.4-0.5 GB, HBM-bound) -- reported beside the headline line, not instead of it.
+    precond=1: the same measurement for the SIMPLE preconditioner (NEXT f1)."""
     import torch
     from synthetic import initial_state, make_problem
     p = make_problem(config)
     phi, rho, s = initial_state(p, 1.0)
-    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream,
+                     opts=pb.default_solver_opts(precond=precond))
     xs = [torch.tensor(x, device=dev) for x in (phi, rho, s)]
     last = {}
 
@@ -270,12 +272,14 @@ def scale_point(pb, config, dev, stream, steps=2):
     step()
     roof, _, _, _ = roofline_of(ctx, ctx.prof_stop(), config)
     st = last["st"]
-    out = {"workload": f"{config}: first IPM Newton system (A19 point, mu=1), eps_out=1e-10", "nbar": ctx.nbar,
+    pre = "SIMPLE" if precond == 1 else "BB"
+    out = {"workload": f"{config}: first IPM Newton system (A19 point, mu=1), {pre}, eps_out=1e-10", "nbar": ctx.nbar,
            "K": ctx.K, "n_plus_m": ctx.n + ctx.m, "value": 1.0 / t, "unit": "solves/s", "ms_per_step": 1e3 * t,
            "unknowns_per_s": (ctx.n + ctx.m) / t, "steps": steps, "warmup": 1,
            "solve": {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "inner_A_its_total",
                                         "converged", "rel_res")},
            "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms")},
+           "ms_per_outer": round(st["t_krylov_ms"] / max(1, st["outer_its"]), 4),
            "roofline": roof}
     ctx.close()
     return out
@@ -416,6 +420,13 @@ def main():
         except Exception as ex:                          # the headline line must still print
             scale = {"error": str(ex)[:200]}
 
+    simple = None      # NEXT f1: the SIMPLE preconditioner on the headline config
+    if rank == 0 and world == 1 and not args.no_profile:
+        try:
+            simple = scale_point(pb, args.config, dev, stream, precond=1)
+        except Exception as ex:
+            simple = {"error": str(ex)[:200]}
+
     protocol = None
     if rank == 0 and world == 1 and args.ipm_config and not args.no_profile:
         try:
@@ -453,6 +464,7 @@ def main():
             "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms", "t_graph_ms")},
             "roofline": roof,
             "hbm_scale_point": scale,
+            "simple_point": simple,
             "ipm_protocol": protocol,
             "cpu_baseline": cpu,
             "clocks": clocks,
