@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--warm", type=int, default=1)
+    ap.add_argument("--precond", type=int, default=0, help="0 = BB, 1 = SIMPLE (NEXT f1)")
     a = ap.parse_args()
     import torch
     import paper_2209_00315_b200 as pb
@@ -26,7 +27,8 @@ def main():
     p = make_problem(a.config)
     phi, rho, s = initial_state(p, 1.0)
     stream = torch.cuda.current_stream()
-    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=stream.cuda_stream,
+                     opts=pb.default_solver_opts(precond=a.precond))
     dev = [torch.tensor(x, device="cuda") for x in (phi, rho, s)]
 
     def step():
