@@ -723,6 +723,7 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailT(const TailTArgs* __restrict__
     const long long w0 = g0 >> 5, ws = gs >> 5;
     for (long long row = w0; row < n; row += ws) {
       double acc = 0.0;
+#pragma unroll 8
       for (int j = lane; j < n; j += 32) acc += T->cinv[(size_t)row * n + j] * C.b[j];
       acc = warp_sum(acc);
       if (lane == 0) C.xo[row] = acc;
@@ -856,6 +857,7 @@ __global__ void k_dense_mv(int n, const double* __restrict__ A, const double* __
   int lane = threadIdx.x & 31;
   if (warp >= n) return;
   double acc = 0.0;
+#pragma unroll 8   // loads issued ahead; the single accumulator keeps the summation order
   for (int j = lane; j < n; j += 32) acc += A[(size_t)warp * n + j] * b[j];
   acc = warp_sum(acc);
   if (lane == 0) x[warp] = acc;
