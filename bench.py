@@ -270,7 +270,7 @@ def scale_point(pb, config, dev, stream, steps=2, precond=0):
     t = e0.elapsed_time(e1) / 1e3 / steps
     ctx.prof_start()
     step()
-    roof, _, _, _ = roofline_of(ctx, ctx.prof_stop(), config)
+    roof, _, _, _ = roofline_of(ctx, ctx.prof_stop(), config + ("-SIMPLE" if precond == 1 else ""))
     st = last["st"]
     pre = "SIMPLE" if precond == 1 else "BB"
     out = {"workload": f"{config}: first IPM Newton system (A19 point, mu=1), {pre}, eps_out=1e-10", "nbar": ctx.nbar,
