@@ -136,3 +136,25 @@ def test_ipm_parity_compression_T2c():
     ctx.set_state(phi, rho, s, 1.0)
     st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=2.0 ** -10))
     _ipm_compare(log, res.log, st, res.kinetic_energy)
+
+
+@pytest.mark.parametrize("name,L,K", [("T0", 0, 1), ("T0", 0, 2), ("T1", 1, 1)])
+def test_simple_degenerate_sizes(name, L, K):
+    """SIMPLE on the degenerate sizes (K = 1: Ŝ has one time block; L = 0: 8 coarse cells):
+    the dense coarsest is level 0, directions to 1e-8, counts +-1."""
+    from threadpoolctl import threadpool_limits
+    pb = _gpu()
+    p = make_problem(name, L=L, K=K)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=7, mu=0.1)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, opts=pb.default_solver_opts(precond=1))
+    ctx.set_state(phi, rho, s, 0.1)
+    ctx.assemble()
+    assert ctx.amg_info(1) == [d.m]
+    dphi, drho, ds, st = ctx.solve()
+    with threadpool_limits(1):
+        S = SimpleSolver(d, phi, rho, s, 0.1, SolverOpts(precond="simple"))
+        ophi, orho, os_ = S.solve()
+    assert st["converged"] == S.stats["converged"] and abs(st["outer_its"] - S.stats["outer_its"]) <= 1
+    for a, b in ((dphi, ophi), (drho, orho), (ds, os_)):
+        assert np.linalg.norm(a - b) <= 1e-8 * max(np.linalg.norm(b), 1e-300)
