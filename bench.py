@@ -285,9 +285,10 @@ def scale_point(pb, config, dev, stream, steps=2, precond=0):
     return out
 
 
-def ipm_protocol(pb, config, dev):
+def ipm_protocol(pb, config, dev, simple_below_mu=0.0):
     """BASELINE configs[0]'s own protocol on the GPU: the full interior-point run (A17-A20,
-    mu 1 -> 2^-26) -- every Newton system of the trajectory, not just the first."""
+    mu 1 -> 2^-26) -- every Newton system of the trajectory, not just the first.
+    simple_below_mu > 0: the BB -> SIMPLE hybrid (A34, NEXT f1)."""
     import torch
     from synthetic import initial_state, make_problem
     p = make_problem(config)
@@ -295,11 +296,12 @@ def ipm_protocol(pb, config, dev):
     ctx.set_state(*initial_state(p, 1.0), 1.0)
     torch.cuda.synchronize(dev)
     t = time.perf_counter()
-    st, log = ctx.ipm_run(pb.default_ipm_opts())
+    st, log = ctx.ipm_run(pb.default_ipm_opts(simple_below_mu=simple_below_mu))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t
     ctx.close()
-    return {"workload": f"{config}: full IPM, mu 1 -> 2^-26 (A17-A20), eps_out=1e-10", "n_systems": st["n_systems"],
+    pre = f", SIMPLE below mu={simple_below_mu:g}" if simple_below_mu > 0 else ", BB"
+    return {"workload": f"{config}: full IPM, mu 1 -> 2^-26 (A17-A20){pre}, eps_out=1e-10", "n_systems": st["n_systems"],
             "total_outer": st["total_outer"], "n_capped": st["n_unconverged"], "final_mu": st["final_mu"],
             "kinetic_energy": st["kinetic_energy"], "wall_s": round(wall, 3),
             "solves_per_s": st["n_systems"] / wall, "timing": "host wall clock around bbot_ipm_run"}
@@ -427,12 +429,16 @@ def main():
         except Exception as ex:
             simple = {"error": str(ex)[:200]}
 
-    protocol = None
+    protocol = hybrid = None
     if rank == 0 and world == 1 and args.ipm_config and not args.no_profile:
         try:
             protocol = ipm_protocol(pb, args.ipm_config, dev)
         except Exception as ex:
             protocol = {"error": str(ex)[:200]}
+        try:
+            hybrid = ipm_protocol(pb, args.ipm_config, dev, simple_below_mu=0.1)
+        except Exception as ex:
+            hybrid = {"error": str(ex)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -466,6 +472,7 @@ def main():
             "hbm_scale_point": scale,
             "simple_point": simple,
             "ipm_protocol": protocol,
+            "ipm_protocol_hybrid": hybrid,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
