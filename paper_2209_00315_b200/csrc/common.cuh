@@ -203,6 +203,29 @@ __device__ __forceinline__ double block_sum(double v) {
   if (w == 0) v = warp_sum(v);
   return v;
 }
+// partial[k * parts + blockIdx.x] = block sum of acc[k] for k < cnt (<= NR): per value the
+// same butterfly order as block_sum (bitwise-identical partials), one barrier in total
+// instead of two per value.  Writers fence before red_last_block's counter increment.
+template <int NR>
+__device__ __forceinline__ void block_sum_many(const double (&acc)[NR], int cnt, double* partial, int parts) {
+  __shared__ double shn[NR][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NR; k++)
+    if (k < cnt) {
+      double v = warp_sum(acc[k]);
+      if (lane == 0) shn[k][w] = v;
+    }
+  __syncthreads();
+  for (int k = w; k < cnt; k += nw) {
+    double v = lane < nw ? shn[k][lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) {
+      partial[(size_t)k * parts + blockIdx.x] = v;
+      __threadfence();
+    }
+  }
+}
 __device__ __forceinline__ double block_min(double v) {
   __shared__ double shm[32];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -127,13 +127,7 @@ __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __re
     for (int k = 0; k < NR; k++)
       if (k <= j) acc[k] += V[(size_t)k * n + i] * wi;
   }
-#pragma unroll
-  for (int k = 0; k < NR; k++) {
-    if (k <= j) {
-      double s = block_sum(acc[k]);
-      if (threadIdx.x == 0) R.partial[(size_t)k * R.parts + blockIdx.x] = s;
-    }
-  }
+  block_sum_many<NR>(acc, j + 1, R.partial, R.parts);
   if (!red_last_block(R.counter)) return;
   double* out = which == 0 ? G->h1 : G->h2;
   red_finish(R.partial, R.parts, j + 1, out);
@@ -170,13 +164,7 @@ __global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double*
     for (int k = 0; k < NR; k++)
       if (k <= j) acc[k] += vk[k] * v;
   }
-#pragma unroll
-  for (int k = 0; k < NR; k++) {
-    if (k <= j) {
-      double t = block_sum(acc[k]);
-      if (threadIdx.x == 0) R.partial[(size_t)k * R.parts + blockIdx.x] = t;
-    }
-  }
+  block_sum_many<NR>(acc, j + 1, R.partial, R.parts);
   if (!red_last_block(R.counter)) return;
   red_finish(R.partial, R.parts, j + 1, G->h2);
 }
