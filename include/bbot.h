@@ -68,6 +68,7 @@ typedef struct {
                         * on J = [[A, B^T],[B, -C]], rhs (f; g~); the inner solve is
                         * S-hat = C + B diag(A)^-1 B^T (stored in T's slot, A31/A32) by
                         * GMRES(restart_T) + AMG, eps_T; recovery dphi = x1, drho = x2.   */
+  int coarse_max_S;    /* AMG(S-hat) coarsest: max rows in total [256] (A32)                 */
 } bbot_solver_opts;
 
 typedef struct {

@@ -39,6 +39,7 @@ class SolverOpts:
     coarse_max_T: int = 1024      # rows in total
     exact_inner: bool = False     # pin mode: exact T solve + exact A_k^+ (no AMG)
     precond: str = "bb"           # "bb" (§4.5) or "simple" (§5.3, NEXT row f1)
+    coarse_max_S: int = 256       # AMG(Ŝ) coarsest rows (SIMPLE, A32)
 
 
 class BBSolver:

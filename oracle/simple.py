@@ -13,7 +13,8 @@ so on (r1; r2):
 S̃ z2 = c is solved as Ŝ z2 = -c with Ŝ = -S̃ = C + B Ã^{-1} B^T (SPD, block tridiagonal in
 time, "formed explicitly"), by the inner solver of the T system: GMRES(restart_T)
 right-preconditioned by one AMG V-cycle (mode T, l1-Jacobi, aggregation across time slices
-as AGMG's), relative eps_in = 1e-1, cap maxit_inner (A32).  Outer: FGMRES(restart)
+as AGMG's, dense coarsest <= coarse_max_S = 256 rows), relative eps_in = 1e-1,
+cap maxit_inner (A32).  Outer: FGMRES(restart)
 on J, stopping at eps_out ||(f;g;h)||.  Recovery: δφ = x1, δρ = x2, δs = ρ^{-1}(h - s δρ).
 
 Pins (tests/test_oracle_simple.py): with an exact Ŝ solve, P^{-1} inverts
@@ -64,7 +65,7 @@ class SimpleSolver:
         else:
             # A32: one "slice" -- AMG(Ŝ) aggregates across time as well (at φ = 0, B is the
             # pure time difference and Ŝ has no in-slice couplings at all)
-            self.amgS = amg.setup(self.S, np.zeros(d.m, dtype=np.int64), "T", o.omega_T, o.coarse_max_T)
+            self.amgS = amg.setup(self.S, np.zeros(d.m, dtype=np.int64), "T", o.omega_T, o.coarse_max_S)
 
     def matvec(self, v):
         """J v = (A x + B^T y; B x - C y)."""

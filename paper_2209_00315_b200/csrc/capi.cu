@@ -49,6 +49,7 @@ void check_opts(const bbot_solver_opts& o) {
   BB_REQUIRE(o.coarse_max_A >= 2 && o.coarse_max_A <= 120 && o.coarse_max_T >= 1 && o.coarse_max_T <= 8192,
              BBOT_E_INPUT, "bad coarse sizes");
   BB_REQUIRE(o.precond == 0 || o.precond == 1, BBOT_E_INPUT, "precond must be 0 (BB) or 1 (SIMPLE)");
+  BB_REQUIRE(o.coarse_max_S >= 1 && o.coarse_max_S <= 8192, BBOT_E_INPUT, "bad coarse_max_S");
 }
 
 }  // namespace
@@ -69,6 +70,7 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->coarse_max_A = 64;
   o->coarse_max_T = 1024;
   o->precond = 0;
+  o->coarse_max_S = 256;
 }
 
 void bbot_default_ipm_opts(bbot_ipm_opts* o) {

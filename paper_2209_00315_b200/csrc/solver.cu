@@ -55,7 +55,7 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   AmgWork& w = c->amgw;
   if (c->as.precond == 1) {   // SIMPLE: one hierarchy, on S-hat (the A block is inverted by its diagonal)
     c->amgA.clear();
-    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_T, w);
+    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_S, w);
   } else if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
     amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
     amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);

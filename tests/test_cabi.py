@@ -37,7 +37,7 @@ def test_oracle_defaults_agree_with_library():
     from oracle.bb import SolverOpts
     o, s = pb.default_solver_opts(), SolverOpts()
     for f in ("eps_out", "eps_T", "eps_A", "restart", "maxit", "restart_T", "maxit_inner",
-              "omega_A", "omega_T", "coarse_max_A", "coarse_max_T"):
+              "omega_A", "omega_T", "coarse_max_A", "coarse_max_T", "coarse_max_S"):
         assert getattr(o, f) == getattr(s, f), f
     assert o.precond == 0 and s.precond == "bb"
 
