@@ -187,7 +187,7 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
     L = len(levels)
     H.kcycle = [mode == "A" and L >= KC_MIN_LEVELS and 0 < l < L - 1 and
                 _slice_sizes(levels[l].slice_of_row, nslices).max() <= KC_ROWS for l in range(L)]
-    Ac = levels[-1].A.toarray()
+    Ac = levels[-1].A.toarray() if (mode == "A" or levels[-1].A.shape[0] <= coarse_max) else None
     if mode == "A":
         sl = levels[-1].slice_of_row
         for k in range(nslices):
@@ -195,13 +195,18 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
             blk = Ac[np.ix_(rows, rows)]
             inv = np.linalg.inv(blk[1:, 1:]) if rows.size > 1 else np.zeros((0, 0))
             H.coarse_inv.append((rows, inv))
-    else:
+    elif Ac is not None:
         H.coarse_dense_inv = np.linalg.inv(Ac)
+    # else: coarsening stalled above coarse_max (decoupled rows: e.g. AMG(Ŝ) at φ = 0 collapses
+    # every cell's time line and leaves a diagonal matrix); the coarsest "solve" is then one
+    # l1-Jacobi sweep from zero -- exact for a diagonal matrix (I3, A32)
     return H
 
 
 def _coarse_solve(H: Hierarchy, b):
     if H.mode == "T":
+        if H.coarse_dense_inv is None:                     # stalled coarsening (setup)
+            return H.omega * H.levels[-1].dinv * b
         return H.coarse_dense_inv @ b
     x = np.zeros_like(b)
     for rows, inv in H.coarse_inv:

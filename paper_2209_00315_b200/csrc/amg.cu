@@ -1125,9 +1125,11 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     size_t smem = (size_t)H.cm * 2 * H.cm * sizeof(double);
     BB_CUDA(cudaFuncSetAttribute(k_coarseA_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch(d, k_coarseA_setup, dim3(nslices), dim3(256), smem, (const long long*)H.csptr.p, C.view(), H.cm, H.cinv.p);
+  } else if (C.n > coarse_max) {   // stalled coarsening: Jacobi coarsest (oracle/amg.py)
+    H.cjac = true;
+    H.cm = (int)C.n;
   } else {
     long long n = C.n;
-    BB_REQUIRE(n <= 8192, BBOT_E_INTERNAL, "AMG(T): coarsest level too large");
     H.cm = (int)n;
     DBuf<double> D;
     D.alloc((size_t)n * n, s);
@@ -1164,7 +1166,7 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
   }
   for (size_t l = 1; l < H.lv.size(); l++) build_sell(d, H.lv[l], w);
   // mode T: the coarse tail starts at the first coarse level with <= TAILT_ROWS rows
-  if (mode == 1 && H.lv.size() >= 3) {
+  if (mode == 1 && H.lv.size() >= 3 && !H.cjac) {
     int L = (int)H.lv.size();
     H.tail = 0;
     for (int l = 1; l < L - 1; l++)
@@ -1251,6 +1253,8 @@ static void coarse_solve(Dev& d, AmgHierarchy& H, const double* b, double* x) {
   if (H.mode == 0)
     launch(d, k_coarseA_apply, dim3(H.nslices), dim3(128), 0, (const long long*)H.csptr.p, H.cm,
            (const double*)H.cinv.p, b, x);
+  else if (H.cjac)
+    launch(d, k_jacobi0, dim3(nblocks(C.n, 256)), dim3(256), 0, C.n, (const double*)C.dinv.p, b, H.omega, x);
   else
     launch(d, k_dense_mv, dim3(nblocks((long long)C.n * 32, 256)), dim3(256), 0, (int)C.n,
            (const double*)H.cinv.p, b, x);

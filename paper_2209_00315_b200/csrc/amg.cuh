@@ -184,8 +184,10 @@ struct AmgHierarchy {
   int tail = 0;            // mode A: first level handled by the per-slice tail kernel
   DBuf<char> tail_args;    // the tail kernel's level table (device; TailArgs / TailTArgs)
   int tail_cl = 1;         // cluster size of the tail launch
+  bool cjac = false;       // mode T: coarsening stalled above coarse_max -> the coarsest "solve"
+                           // is one l1-Jacobi sweep from zero (exact on a diagonal matrix)
   bool ready = false;
-  void clear() { lv.clear(); ready = false; tail = 0; tail_cl = 1; }
+  void clear() { lv.clear(); ready = false; tail = 0; tail_cl = 1; cjac = false; }
 };
 
 struct AmgWork {
