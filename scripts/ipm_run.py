@@ -40,7 +40,8 @@ def main():
                             callback=cb)
     wall = time.time() - t
     print(json.dumps({"config": a.config, "n_systems": st["n_systems"], "total_outer": st["total_outer"],
-                      "n_unconverged": st["n_unconverged"], "final_mu": st["final_mu"],
+                      "n_unconverged": st["n_unconverged"], "n_simple_fallback": st["n_simple_fallback"],
+                      "final_mu": st["final_mu"],
                       "kinetic_energy": st["kinetic_energy"], "wall_s": round(wall, 2),
                       "solves_per_s": st["n_systems"] / wall}))
 
