@@ -177,7 +177,8 @@ bbot_status bbot_jp_matvec(bbot_ctx* ctx, const double* x, double* y, bbot_mem m
 bbot_status bbot_bb_apply(bbot_ctx* ctx, const double* r, double* z, bbot_mem mem,
                           int* inner_T_its, int* inner_A_its_max);
 
-/* a5 + a6: FGMRES on (4.17) with the BB preconditioner, then recovery of
+/* a5 + a6: FGMRES on (4.17) with the BB preconditioner (or, after a SIMPLE assembly, on
+ * the saddle-point system with SIMPLE; recovery dphi = x1, drho = x2), then recovery of
  * (dphi, drho, ds); st also reports the timings of the last bbot_assemble.
  * (dphi, drho, ds) ((4.15) with A10, A30).  Outputs may be
  * NULL (the direction is always kept in the context for bbot_newton_update). */
@@ -188,7 +189,8 @@ bbot_status bbot_solve(bbot_ctx* ctx, double* dphi, double* drho, double* ds,
  * last direction, per-slice renormalisation of rho (Remark 3.2). */
 bbot_status bbot_newton_update(bbot_ctx* ctx, double frac_to_boundary, double* alpha);
 
-/* a7: full IPM run from the current state (mu schedule A17, Newton stop A18). */
+/* a7: full IPM run from the current state (mu schedule A17, Newton stop A18); with
+ * o->simple_below_mu > 0 every Newton system at mu below it uses SIMPLE (A34). */
 bbot_status bbot_ipm_run(bbot_ctx* ctx, const bbot_ipm_opts* o, bbot_ipm_stats* st,
                          bbot_ipm_cb cb, void* user);
 
