@@ -106,3 +106,19 @@ def test_hybrid_ipm_reaches_the_same_central_path_point():
     assert all((r["inner_A_its_max"] == 0) == (r["mu"] < thr) for r in b.log)
     assert abs(a.kinetic_energy - b.kinetic_energy) <= 1e-6 * a.kinetic_energy
     assert np.linalg.norm(a.rho - b.rho) <= 1e-4 * np.linalg.norm(a.rho)
+
+
+def test_stalled_coarsening_jacobi_coarsest_is_exact():
+    """I3 / A32: at φ = 0 (A19) B is the pure time difference, so AMG(Ŝ)'s cross-slice
+    aggregation collapses every coarse cell's time line and stalls on a DIAGONAL matrix with
+    one row per cell; the coarsest "solve" (one l1-Jacobi sweep, ω = 1) is then exact."""
+    from oracle import amg
+    p, d = _disc("T2")
+    phi, rho, s = initial_state(p, 1.0)
+    H = amg.setup(S_hat(d, phi, rho, s), np.zeros(d.m, dtype=np.int64), "T", 1.0, 4)
+    C = H.levels[-1].A.toarray()
+    assert H.sizes[-1] == d.nbar and H.coarse_dense_inv is None
+    assert np.count_nonzero(C - np.diag(np.diag(C))) == 0
+    b = np.random.default_rng(2).standard_normal(d.nbar)
+    x = amg._coarse_solve(H, b)
+    assert np.allclose(C @ x, b, rtol=0, atol=1e-12 * np.abs(b).max())
