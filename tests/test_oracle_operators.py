@@ -152,3 +152,89 @@ def test_B_and_Btilde_consistency():
         eB.append(np.linalg.norm(d.B(phi) @ x - ex2) / np.linalg.norm(ex2))
     for e in (eB, eBt):
         assert e[0] < 0.15 and e[1] < 0.6 * e[0] and e[2] < 0.6 * e[1], (eB, eBt)
+
+
+# --------------------------------------------------------------------------- Ã, R̄, DR pins
+def _jittered_disc(L=2, K=2, seed=7):
+    """A jittered A1 mesh (A25 recipe, another seed): λ̄, λ ≠ ½ on almost every edge, so a
+    swapped or rescaled reconstruction weight cannot pass by symmetry."""
+    from synthetic import build_mesh, jitter_mesh
+    v, t = build_mesh(L)
+    v, _ = jitter_mesh(v, t, h=1.0 / 2 ** (L + 1), amp=0.2, seed=seed)
+    nb = t.shape[0]
+    return Discretisation(v, t, K, np.ones(nb), np.ones(nb))
+
+
+def _interior_triangles(g):
+    """Coarse cells whose three edges are all internal (boundary edges are dropped)."""
+    cnt = np.bincount(np.r_[g.ebar_L, g.ebar_R], minlength=g.nbar)
+    return np.nonzero(cnt == 3)[0]
+
+
+def test_Atilde_interior_cell_identity():
+    """Ã_k = Ē_c diag(|ē| R̄ρ^k/|w̄|) Ē_cᵀ "discretizes -∇·(ρ∇)":
+    for u = a·x sampled at the circumcentres and ρ = e_i (one coarse cell),
+        uᵀ Ã(e_i) u = Σ_{ē ⊂ ∂i} |ē| (R̄e_i)_ē (a·n_ē)² |w̄_ē| = Σ_ē |ē| d(cc_i, ē) (a·n_ē)² = |c̄_i| |a|²
+    exactly, because (R̄e_i)_ē = d(cc_i, ē)/|w̄| (A3 on the coarse mesh) and, by the divergence
+    theorem with the circumcentre's perpendicular feet at the edge midpoints,
+    Σ_ē |ē| d(cc_i, ē) n nᵀ = |c̄_i| I for every triangle with three internal edges.
+    A swapped λ̄ (1 - λ̄), or Ã scaled by any factor, breaks it."""
+    d = _jittered_disc()
+    g = d.g
+    lam = g.lam_bar
+    assert np.abs(lam - 0.5).max() > 0.05            # the mesh really is asymmetric
+    rng = np.random.default_rng(11)
+    inner = _interior_triangles(g)
+    assert inner.size > g.nbar // 2
+    for a in (np.array([1.0, 0.0]), np.array([0.0, 1.0]), rng.standard_normal(2)):
+        u = g.cc @ a
+        for i in inner:
+            rho = np.zeros(d.K * d.nbar)
+            rho[i] = 1.0                              # slice 1 = e_i
+            At = d.Atilde_blocks(rho)[0]
+            val = u @ (At @ u)
+            assert abs(val - g.cbar[i] * (a @ a)) <= 1e-12 * g.cbar[i] * (a @ a), (i, val)
+
+
+def test_Atilde_symmetric_zero_rowsum_psd():
+    """Ã_k = Ãᵀ_k, Ã_k 1 = 0 and PSD (a weighted graph Laplacian)."""
+    d = _jittered_disc()
+    rho = np.random.default_rng(3).uniform(0.1, 2.0, d.K * d.nbar)
+    for At in d.Atilde_blocks(rho):
+        assert abs(At - At.T).max() < 1e-15
+        assert abs(At @ np.ones(d.nbar)).max() < 1e-13 * abs(At).max()
+        ev = np.linalg.eigvalsh(At.toarray())
+        assert ev.min() > -1e-12 * ev.max()
+
+
+def test_DR_interior_cell_identity():
+    """The fine reconstruction (A3: λ_σ = d(x_L,σ)/|w|): for φ = a·x sampled at the
+    fine cell points, (DR (grad φ)²)_i = Σ_σ R_E[σ,i] |w_σ||e_σ| (a·n_σ)² = Σ_{kites f ⊂ i}
+    Σ_{σ ∋ f} |e_σ| d(x_f, σ) (a·n_σ)² = |c̄_i| |a|²  for coarse cells with three internal
+    edges (each kite is cyclic with its anchor (v+cc)/2 as circumcentre, A2, so the same
+    divergence-theorem identity holds kite by kite).  This pins λ, R_E and DR (a swapped λ,
+    a dropped |w| or |e|, or a factor fails it); it is the consistency DR(∇φ)² ≈ |c̄||∇φ|²
+    behind the kinetic energy (1.1)."""
+    d = _jittered_disc()
+    g = d.g
+    assert np.abs(g.lam[g.e_type == 1] - 0.5).max() > 0.05
+    inner = _interior_triangles(g)
+    rng = np.random.default_rng(12)
+    for a in (np.array([1.0, 0.0]), np.array([0.0, 1.0]), rng.standard_normal(2)):
+        phi = g.x @ a
+        gp = d.grad @ phi
+        val = d.DR @ (gp ** 2)
+        assert np.allclose(val[inner], g.cbar[inner] * (a @ a), rtol=1e-12, atol=0)
+        # and the same identity through the kinetic energy D12 for a slice-constant-in-time
+        # linear φ with ρ ≡ 1 on the interior cells: KE-per-slice = ½ Σ_i ρ_i |c̄_i| |a|²
+
+
+def test_Atilde_reading_is_psd_sign():
+    """Sign reading (DESIGN §2 A35): the printed 'div · diag · grad' of P:1619-1623 is read as
+    +Ē_c diag(·) Ē_cᵀ, i.e. Ã discretises -∇·(ρ∇) (P:1617 'discretizes -Δρ'), PSD: for a
+    nonconstant u, uᵀÃu > 0 -- with the other sign the BB Schur approximation T has negative
+    diagonal entries (the time Laplacian part is PSD, test_T_at_zero_potential_is_time_laplacian)."""
+    d = _jittered_disc()
+    rho = np.ones(d.K * d.nbar)
+    u = d.g.cc[:, 0]
+    assert u @ (d.Atilde_blocks(rho)[0] @ u) > 0.1 * d.area
