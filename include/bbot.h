@@ -116,9 +116,8 @@ typedef struct {
   double final_mu;
   double kinetic_energy;    /* D12 at the final state                                       */
   double wall_ms;
-  int n_simple_fallback;    /* SIMPLE systems solved with BB instead: AMG(S-hat) could not be
-                             * built (a cross-slice coarse row wider than the Galerkin
-                             * capacity, BBOT_E_INTERNAL; A34)                            */
+  int n_simple_fallback;    /* always 0 (kept for ABI stability): AMG(S-hat) coarse rows have no
+                             * width cap any more, so every SIMPLE system is solved with SIMPLE */
 } bbot_ipm_stats;
 
 void bbot_default_solver_opts(bbot_solver_opts* o);
@@ -185,6 +184,23 @@ bbot_status bbot_bb_apply(bbot_ctx* ctx, const double* r, double* z, bbot_mem me
 bbot_status bbot_solve(bbot_ctx* ctx, double* dphi, double* drho, double* ds,
                        bbot_solve_stats* st, bbot_mem mem);
 
+/* solve(rhs) -> direction (north star): the Newton system (3.1)
+ * of the last bbot_assemble with a CALLER-GIVEN right-hand side:
+ *   [[A, B^T, 0], [B, 0, Mbar], [0, diag(s), diag(rho)]] (dphi; drho; ds) = (f; g; h).
+ * f: n, g: m, h: m (slice-major, as the state; `mem` says host or device).  ds is
+ * eliminated: g~ = g - Mbar h / rho; FGMRES (BB: on (4.17) with rhs (f; P g~),
+ * P:1424-1448; SIMPLE: on the saddle-point system with rhs (f; g~)) stops at
+ * eps_out ||(f;g;h)||_2; recovery as bbot_solve.  Solvability: (3.1) is
+ * singular along (1;0;0) (Remark 3.1), so sum_k 1^T f^k must vanish.  (4.17)
+ * needs 1^T f^k = 0 slice by slice (A30); the slice masses m_k = c-bar^T drho^k are fixed
+ * first from the phi rows' slice sums (m_k = m_{k-1} - dt 1^T f^k) and the rest is solved
+ * through (4.17).  For an f outside the range the solve runs to the cap (converged = 0).
+ * The operator is NOT rebuilt: it stays the one of the last assembly; the next bbot_solve
+ * re-derives the Newton right-hand side
+ * itself.  The direction is not kept for bbot_newton_update. */
+bbot_status bbot_solve_rhs(bbot_ctx* ctx, const double* f, const double* g, const double* h, double* dphi,
+                           double* drho, double* ds, bbot_solve_stats* st, bbot_mem mem);
+
 /* a7: step length (fraction to boundary, A20), update of (phi, rho, s) with the
  * last direction, per-slice renormalisation of rho (Remark 3.2). */
 bbot_status bbot_newton_update(bbot_ctx* ctx, double frac_to_boundary, double* alpha);
@@ -202,6 +218,11 @@ bbot_status bbot_kinetic_energy(bbot_ctx* ctx, double* ke);
 bbot_status bbot_get_T(bbot_ctx* ctx, long long* nnz, long long* rowptr, int* cols, double* vals);
 /* which: 0 = AMG(A), 1 = AMG(T).  sizes: >= 32 entries. */
 bbot_status bbot_amg_info(bbot_ctx* ctx, int which, int* nlevels, long long* sizes);
+/* level `level` of hierarchy `which`: rows n, stored nnz (-1 on level 0, which is read
+ * through the operator's own view, not stored), coarse rows nc (0 at the coarsest), and
+ * the first level handled by the per-slice tail kernel (0: none).  For byte models. */
+bbot_status bbot_amg_level_info(bbot_ctx* ctx, int which, int level, long long* n, long long* nnz, long long* nc,
+                                int* tail);
 /* fine-row -> coarse-row map of level `level` (host, length sizes[level]). */
 bbot_status bbot_amg_agg(bbot_ctx* ctx, int which, int level, int* agg);
 /* one V-cycle x = M^-1 b on level 0 of hierarchy `which` (length n or m). */
@@ -239,7 +260,8 @@ bbot_status bbot_set_exec_mode(bbot_ctx* ctx, int use_graph);
 /* Per-launch profiler: between start and stop every kernel launch is bracketed
  * by CUDA events on the context stream (adds ~2 event records per launch; use
  * for kernel shares, not for the headline timing).  stop writes a text table
- * "demangled-name<TAB>launches<TAB>total_ms" into buf (NUL-terminated,
+ * "demangled-name<TAB>launches<TAB>total_ms<TAB>grid-CTAs" (one line per kernel and
+ * grid size) into buf (NUL-terminated,
  * truncated to buflen) and the required size into *needed. */
 bbot_status bbot_prof_start(bbot_ctx* ctx);
 bbot_status bbot_prof_stop(bbot_ctx* ctx, char* buf, long long buflen, long long* needed);

@@ -108,6 +108,35 @@ class BBSolver:
         self.sol = sol
         return self.recover(sol)
 
+    def solve_rhs(self, f, g, h):
+        """solve(rhs) -> direction for the Newton system (3.1) of this state with a
+        caller-given right-hand side (f; g; h), solvable iff Σ_k 1ᵀf^k = 0 (the left kernel of
+        J is (1;0;0), Remark 3.1).  (4.17) needs 1ᵀf^k = 0 slice by slice (A30), so the mass
+        part of δρ is taken first: summing the k-th φ row of (3.1),
+            1ᵀ(A_kδφ^k + (Bᵀδρ)^k) = c̄ᵀ(δρ^{k-1} - δρ^k)/Δt = 1ᵀf^k   (1ᵀA_k = 0, D6),
+        fixes the slice masses m_k = c̄ᵀδρ^k = m_{k-1} - Δt 1ᵀf^k (m_0 = 0);  with
+        δρ₀^k = (m_k/|Ω|)·1 the remainder δρ' = δρ - δρ₀ solves (3.1) with
+        (f - Bᵀδρ₀; g; h - s⊙δρ₀), whose φ rows have zero slice sums, by the BB solve
+        (4.17) + recovery; then δρ = δρ' + δρ₀.  Stop at ε‖(f;g;h)‖."""
+        d = self.d
+        K = d.K
+        f = np.asarray(f, float)
+        g = np.asarray(g, float)
+        h = np.asarray(h, float)
+        Sf = f.reshape(K + 1, d.N).sum(axis=1)
+        mk = -d.dt * np.cumsum(Sf)[:K]                                    # m_1 .. m_K
+        drho0 = np.repeat(mk / d.area, d.nbar)
+        self.f = f - self.BT @ drho0
+        self.g = g
+        self.h = h - self.s * drho0
+        self.gt = self.g - np.tile(d.Mbar, K) * self.h / self.rho         # g̃ (P:548)
+        self.scale = float(np.sqrt(f @ f + g @ g + h @ h))
+        self.rhs = np.concatenate([self.f, d.P(self.gt)])
+        self.inner_T_its = 0
+        self.inner_A_its = []
+        dphi, drho, ds = self.solve()
+        return dphi, drho + drho0, ds
+
     def recover(self, sol):
         d = self.d
         K, N, n = d.K, d.N, d.n

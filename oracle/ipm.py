@@ -60,9 +60,11 @@ def res_norm(d, phi, rho, s, mu):
     return float(np.sqrt(a @ a + b @ b + c @ c))
 
 
-def newton_step(d: Discretisation, phi, rho, s, mu, opts: SolverOpts, tau: float):
+def newton_step(d: Discretisation, phi, rho, s, mu, opts: SolverOpts, tau: float, keep=None):
     S = (SimpleSolver if opts.precond == "simple" else BBSolver)(d, phi, rho, s, mu, opts)
     dphi, drho, ds = S.solve()
+    if keep is not None:            # test hook: the system solved and its direction
+        keep.update(state=(phi, rho, s), mu=mu, opts=opts, direction=(dphi, drho, ds))
     alpha = step_length(rho, s, drho, ds, tau)
     phi = phi + alpha * dphi
     rho = renormalise(d, rho + alpha * drho)
@@ -94,7 +96,10 @@ class IpmResult:
 
 
 def ipm_run(d: Discretisation, phi, rho, s, ipm: IpmOpts | None = None,
-            opts: SolverOpts | None = None, callback=None) -> IpmResult:
+            opts: SolverOpts | None = None, callback=None, keep_systems: bool = False) -> IpmResult:
+    """keep_systems: every log record also carries the Newton system it solved
+    ("system": dict(state=(phi, rho, s), mu, opts, direction)) -- test infrastructure
+    for per-system parity along the oracle's own trajectory."""
     ipm = ipm or IpmOpts()
     opts = opts or SolverOpts()
     F0 = res_norm(d, phi, rho, s, ipm.mu0)
@@ -106,9 +111,12 @@ def ipm_run(d: Discretisation, phi, rho, s, ipm: IpmOpts | None = None,
             o_mu = opts if mu >= ipm.mu_tight else replace(opts, eps_A=min(opts.eps_A, ipm.eps_A_tight))
             if mu < ipm.simple_below_mu:
                 o_mu = replace(o_mu, precond="simple")
-            phi, rho, s, alpha, st = newton_step(d, phi, rho, s, mu, o_mu, ipm.frac_to_boundary)
+            keep = {} if keep_systems else None
+            phi, rho, s, alpha, st = newton_step(d, phi, rho, s, mu, o_mu, ipm.frac_to_boundary, keep)
             r = res_norm(d, phi, rho, s, mu)
             rec = dict(mu=mu, newton=it, alpha=alpha, res=r, **st)
+            if keep_systems:
+                rec["system"] = keep
             log.append(rec)
             if callback:
                 callback(rec)

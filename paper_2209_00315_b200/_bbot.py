@@ -88,12 +88,14 @@ _sigs = {
     "bbot_jp_matvec": (C.c_int, [_P, _P, _P, C.c_int]),
     "bbot_bb_apply": (C.c_int, [_P, _P, _P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bbot_solve": (C.c_int, [_P, _P, _P, _P, C.POINTER(SolveStats), C.c_int]),
+    "bbot_solve_rhs": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.POINTER(SolveStats), C.c_int]),
     "bbot_newton_update": (C.c_int, [_P, C.c_double, _D]),
     "bbot_ipm_run": (C.c_int, [_P, C.POINTER(IpmOpts), C.POINTER(IpmStats), IPM_CB, C.c_void_p]),
     "bbot_kinetic_energy": (C.c_int, [_P, _D]),
     "bbot_get_T": (C.c_int, [_P, C.POINTER(C.c_longlong), _P, _P, _P]),
     "bbot_amg_info": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_longlong)]),
     "bbot_amg_agg": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "bbot_amg_level_info": (C.c_int, [_P, C.c_int, C.c_int] + [C.POINTER(C.c_longlong)] * 3 + [C.POINTER(C.c_int)]),
     "bbot_amg_vcycle": (C.c_int, [_P, C.c_int, _P, _P, C.c_int]),
     "bbot_launch_count": (C.c_longlong, [_P]),
     "bbot_set_exec_mode": (C.c_int, [_P, C.c_int]),
@@ -263,6 +265,21 @@ class Context:
                                    C.byref(st), mem))
         return dphi, drho, ds, st.as_dict()
 
+    def solve_rhs(self, f, g, h, dphi=None, drho=None, ds=None):
+        """solve(rhs) -> direction: the Newton system (3.1) of the last assembly with a
+        caller-given (f; g; h) (bbot_solve_rhs).  numpy inputs -> numpy outputs; torch
+        device tensors (outputs must be given) -> the direction stays on the GPU."""
+        host = isinstance(f, np.ndarray)
+        if host:
+            f, g, h = (np.ascontiguousarray(a, dtype=np.float64) for a in (f, g, h))
+            dphi, drho, ds = np.empty(self.n), np.empty(self.m), np.empty(self.m)
+        st = SolveStats()
+        fp, mem = _ptr(f, self.n)
+        self._check(lib.bbot_solve_rhs(self._h, fp, _ptr(g, self.m)[0], _ptr(h, self.m)[0],
+                                       _ptr(dphi, self.n, True)[0], _ptr(drho, self.m, True)[0],
+                                       _ptr(ds, self.m, True)[0], C.byref(st), mem))
+        return dphi, drho, ds, st.as_dict()
+
     def solve_stats_only(self):
         st = SolveStats()
         self._check(lib.bbot_solve(self._h, None, None, None, C.byref(st), BBOT_MEM_DEVICE))
@@ -309,6 +326,16 @@ class Context:
         self._check(lib.bbot_amg_info(self._h, which, C.byref(nl), sizes))
         return [sizes[i] for i in range(nl.value)]
 
+    def amg_levels(self, which):
+        """[(n, nnz, nc)] per level (nnz -1 on level 0) and the tail's first level."""
+        out, tail = [], C.c_int()
+        for lvl in range(len(self.amg_info(which))):
+            n, nnz, nc = C.c_longlong(), C.c_longlong(), C.c_longlong()
+            self._check(lib.bbot_amg_level_info(self._h, which, lvl, C.byref(n), C.byref(nnz), C.byref(nc),
+                                                C.byref(tail)))
+            out.append((n.value, nnz.value, nc.value))
+        return out, tail.value
+
     def amg_agg(self, which, level):
         sizes = self.amg_info(which)
         out = np.empty(sizes[level], dtype=np.int32)
@@ -343,13 +370,15 @@ class Context:
     def prof_start(self):
         self._check(lib.bbot_prof_start(self._h))
 
-    def prof_stop(self):
-        """-> {kernel name: (launches, total_ms)}"""
+    def prof_stop(self, by_grid=False):
+        """-> {kernel name: (launches, total_ms)}; by_grid: {(name, grid CTAs): (launches, ms)}"""
         need = C.c_longlong()
-        buf = C.create_string_buffer(1 << 20)
+        buf = C.create_string_buffer(1 << 22)
         self._check(lib.bbot_prof_stop(self._h, buf, len(buf), C.byref(need)))
         out = {}
         for line in buf.value.decode(errors="replace").splitlines():
-            name, cnt, ms = line.rsplit("\t", 2)
-            out[name] = (int(cnt), float(ms))
+            name, cnt, ms, grid = line.rsplit("\t", 3)
+            key = (name, int(grid)) if by_grid else name
+            c0, m0 = out.get(key, (0, 0.0))
+            out[key] = (c0 + int(cnt), m0 + float(ms))
         return out

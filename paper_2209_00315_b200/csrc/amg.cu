@@ -15,7 +15,7 @@ namespace bbot {
 constexpr double AMG_TAU = 1e-8;        // near-tie tolerance (relative)
 constexpr double AMG_DECOUPLED = 1e-10; // rows with max strength <= this*|a_ii| do not propose
 constexpr int MATCH_ROUNDS = 16;
-constexpr int GAL_CAP = 256;            // max distinct columns of a coarse row
+constexpr int GAL_LOCAL = 48;           // coarse rows up to this many entries merge in local arrays
 constexpr int MAX_LEVELS = 25;
 constexpr int BS = 256;
 
@@ -206,16 +206,30 @@ __global__ void k_sort_members(long long nc, const long long* __restrict__ mptr,
 }
 
 // ------------------------------------------------------------ Galerkin
-template <class V, bool FILL>
-__global__ void k_galerkin(V v, long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
-                           const int* __restrict__ agg, int* cnt, const long long* __restrict__ rp, int* ci,
-                           double* cv, int* err) {
+// Coarse row I of A_c = P^T A P: the union of the member rows' columns mapped through agg,
+// values summed in (member, entry) order, columns ascending.  Rows whose upper bound
+// ub[I] = sum of the member row lengths fits GAL_LOCAL are merged in registers/local
+// memory; wider rows (dense coarse graphs, e.g. AMG(S-hat) across time) are merged in a
+// global scratch segment of ub[I] entries at goff[I] -- no width cap.
+template <class V>
+__global__ void k_gal_ub(V v, long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
+                         long long* ub) {
   long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= nc) return;
-  int cols[GAL_CAP];
-  double vals[GAL_CAP];
+  long long u = 0;
+  for (long long p = mptr[I]; p < mptr[I + 1]; p++) v.row(midx[p], [&](long long, double) { u++; });
+  ub[I] = u;
+}
+__global__ void k_gal_big(long long nc, const long long* __restrict__ ub, long long* big) {
+  long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (I < nc) big[I] = ub[I] > GAL_LOCAL ? ub[I] : 0;
+}
+
+template <class V>
+__device__ __forceinline__ int gal_merge(const V& v, long long I, const long long* __restrict__ mptr,
+                                         const int* __restrict__ midx, const int* __restrict__ agg, int* cols,
+                                         double* vals) {
   int len = 0;
-  bool over = false;
   for (long long p = mptr[I]; p < mptr[I + 1]; p++) {
     long long m = midx[p];
     v.row(m, [&](long long c, double a) {
@@ -228,17 +242,31 @@ __global__ void k_galerkin(V v, long long nc, const long long* __restrict__ mptr
       }
       if (lo < len && cols[lo] == J) {
         vals[lo] += a;
-      } else if (len < GAL_CAP) {
+      } else {
         for (int q = len; q > lo; q--) { cols[q] = cols[q - 1]; vals[q] = vals[q - 1]; }
         cols[lo] = J;
         vals[lo] = a;
         len++;
-      } else {
-        over = true;
       }
     });
   }
-  if (over) atomicExch(err, 1);
+  return len;
+}
+
+// BIG = false: rows with ub <= GAL_LOCAL (local arrays); BIG = true: the others (scratch)
+template <class V, bool FILL, bool BIG>
+__global__ void k_galerkin(V v, long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
+                           const int* __restrict__ agg, const long long* __restrict__ ub,
+                           const long long* __restrict__ goff, int* gcols, double* gvals, int* cnt,
+                           const long long* __restrict__ rp, int* ci, double* cv) {
+  long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= nc) return;
+  if ((ub[I] > GAL_LOCAL) != BIG) return;
+  int lcols[BIG ? 1 : GAL_LOCAL];
+  double lvals[BIG ? 1 : GAL_LOCAL];
+  int* cols = BIG ? gcols + goff[I] : lcols;
+  double* vals = BIG ? gvals + goff[I] : lvals;
+  int len = gal_merge(v, I, mptr, midx, agg, cols, vals);
   if (!FILL) {
     cnt[I] = len;
   } else {
@@ -983,19 +1011,32 @@ void galerkin(Dev& d, const V& v, long long nc, const long long* mptr, const int
               AmgLevel& out, AmgWork& w) {
   cudaStream_t s = d.stream;
   grow(w.cnt, nc, s);
-  grow(w.err, 1, s);
-  BB_CUDA(cudaMemsetAsync(w.err.p, 0, sizeof(int), s));
+  grow(w.ub, nc, s);
+  grow(w.goff, nc + 1, s);
   unsigned nb = nblocks(nc, 128);
-  launch(d, k_galerkin<V, false>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, agg, w.cnt.p,
-         (const long long*)nullptr, (int*)nullptr, (double*)nullptr, w.err.p);
+  launch(d, k_gal_ub<V>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, w.ub.p);
+  launch(d, k_gal_big, dim3(nb), dim3(128), 0, nc, (const long long*)w.ub.p, w.goff.p);
+  exclusive_scan(d, w.goff.p, w.goff.p, nc, w.ws);
+  long long gtot = read_scalar(d, w.goff.p + nc);
+  if (gtot > 0) {
+    grow(w.gcols, gtot, s);
+    grow(w.gvals, gtot, s);
+  }
+  auto pass = [&](auto fill, int* cnt, const long long* rp, int* ci, double* cv) {
+    constexpr bool F = decltype(fill)::value;
+    launch(d, k_galerkin<V, F, false>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, agg, (const long long*)w.ub.p,
+           (const long long*)w.goff.p, w.gcols.p, w.gvals.p, cnt, rp, ci, cv);
+    if (gtot > 0)
+      launch(d, k_galerkin<V, F, true>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, agg, (const long long*)w.ub.p,
+             (const long long*)w.goff.p, w.gcols.p, w.gvals.p, cnt, rp, ci, cv);
+  };
+  pass(std::false_type{}, w.cnt.p, (const long long*)nullptr, (int*)nullptr, (double*)nullptr);
   out.rp.alloc(nc + 1, s);
   exclusive_scan_i32(d, w.cnt.p, out.rp.p, nc, w.ws);
   long long nnz = read_scalar(d, out.rp.p + nc);
-  BB_REQUIRE(read_scalar(d, w.err.p) == 0, BBOT_E_INTERNAL, "AMG Galerkin: coarse row wider than GAL_CAP");
   out.ci.alloc(std::max(1LL, nnz), s);
   out.v.alloc(std::max(1LL, nnz), s);
-  launch(d, k_galerkin<V, true>, dim3(nb), dim3(128), 0, v, nc, mptr, midx, agg, (int*)nullptr,
-         (const long long*)out.rp.p, out.ci.p, out.v.p, w.err.p);
+  pass(std::true_type{}, (int*)nullptr, (const long long*)out.rp.p, out.ci.p, out.v.p);
   out.n = nc;
 }
 

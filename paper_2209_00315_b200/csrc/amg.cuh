@@ -193,6 +193,9 @@ struct AmgHierarchy {
 struct AmgWork {
   DBuf<int> free_, prop, partner, flag, cnt;
   DBuf<long long> cidx, ws, lptr;
+  DBuf<long long> ub, goff;      // Galerkin: per coarse row entry bound, scratch offsets
+  DBuf<int> gcols;
+  DBuf<double> gvals;
   DBuf<int> err;
 };
 

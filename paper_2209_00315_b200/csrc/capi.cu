@@ -102,15 +102,13 @@ bbot_status bbot_create(const double* vertices, int nv, const int* tris, int nt,
     c->dev.stream = (cudaStream_t)stream;
     int devid = 0;
     BB_CUDA(cudaGetDevice(&devid));
-    {   // keep freed stream-ordered memory in the pool: the AMG hierarchies are rebuilt every
-        // Newton step, and a release threshold of 0 would unmap/remap them at every sync
-      cudaMemPool_t pool;
-      BB_CUDA(cudaDeviceGetDefaultMemPool(&pool, devid));
-      unsigned long long thr = ~0ULL;
-      BB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-      // the AMG(A) tail kernel recurses through the K-cycle levels (depth <= 2 x levels)
+    c->devid = devid;
+    device_pool();   // the library's private pool on this device (common.cu)
+    {   // the AMG(A) tail kernel recurses through the K-cycle levels (depth <= 2 x levels);
+        // the previous limit is restored by bbot_destroy
       size_t stk = 0;
       BB_CUDA(cudaDeviceGetLimit(&stk, cudaLimitStackSize));
+      c->stack_prev = stk;
       if (stk < 4096) BB_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 4096));
     }
     BB_CUDA(cudaDeviceGetAttribute(&c->dev.num_sms, cudaDevAttrMultiProcessorCount, devid));
@@ -161,8 +159,10 @@ void bbot_destroy(bbot_ctx* c) {
   drop_dist(c);
   cudaStream_t s2 = c->dev2.stream;
   if (s2) cudaStreamSynchronize(s2);
+  size_t stk = c->stack_prev;
   delete c;
   if (s2) cudaStreamDestroy(s2);
+  if (stk > 0 && stk < 4096) cudaDeviceSetLimit(cudaLimitStackSize, stk);
 }
 
 const char* bbot_last_error(const bbot_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -294,10 +294,36 @@ bbot_status bbot_solve(bbot_ctx* c, double* dphi, double* drho, double* ds, bbot
   API_BEGIN(c)
   bbot_solve_stats loc;
   memset(&loc, 0, sizeof(loc));
+  if (c->as.valid && c->as.rhs_user) {   // a bbot_solve_rhs replaced the Newton right-hand side
+    compute_residual(c, true);
+    c->as.rhs_user = false;
+  }
   solve(c, &loc);
   copy_out(c, dphi, c->dphi.p, c->n(), mem);
   copy_out(c, drho, c->drho.p, c->m(), mem);
   copy_out(c, ds, c->ds.p, c->m(), mem);
+  if (st) *st = loc;
+  API_END(c)
+}
+
+bbot_status bbot_solve_rhs(bbot_ctx* c, const double* f, const double* g, const double* h, double* dphi,
+                           double* drho, double* ds, bbot_solve_stats* st, bbot_mem mem) {
+  if (!c || !f || !g || !h) return BBOT_E_INPUT;
+  API_BEGIN(c)
+  BB_REQUIRE(c->as.valid, BBOT_E_ORDER, "bbot_solve_rhs before bbot_assemble");
+  long long n = c->n(), m = c->m();
+  copy_in(c, c->as.f.p, f, n, mem);
+  copy_in(c, c->as.g.p, g, m, mem);
+  copy_in(c, c->as.h.p, h, m, mem);
+  set_user_rhs(c);
+  bbot_solve_stats loc;
+  memset(&loc, 0, sizeof(loc));
+  solve(c, &loc);
+  finish_user_solve(c);
+  c->have_dir = false;     // not a Newton direction of the state: bbot_newton_update refuses it
+  copy_out(c, dphi, c->dphi.p, n, mem);
+  copy_out(c, drho, c->drho.p, m, mem);
+  copy_out(c, ds, c->ds.p, m, mem);
   if (st) *st = loc;
   API_END(c)
 }
@@ -358,16 +384,7 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
       memset(&rec, 0, sizeof(rec));
       // A34: the mu-switched BB -> SIMPLE hybrid
       c->opts.precond = mu < o.simple_below_mu ? 1 : precond0;
-      try {
-        assemble_all(c, nullptr);
-      } catch (const Error& e) {
-        // A34: AMG(S-hat) aggregates across time slices and can exceed the Galerkin row
-        // capacity on strongly anisotropic late-IPM states; that system is solved with BB
-        if (c->opts.precond != 1 || e.status != BBOT_E_INTERNAL) throw;
-        c->opts.precond = 0;
-        assemble_all(c, nullptr);
-        S.n_simple_fallback++;
-      }
+      assemble_all(c, nullptr);
       solve(c, &rec.solve);
       rec.alpha = newton_update(c, o.frac_to_boundary);
       c->have_dir = false;
@@ -446,6 +463,19 @@ bbot_status bbot_amg_info(bbot_ctx* c, int which, int* nlevels, long long* sizes
   return BBOT_OK;
 }
 
+bbot_status bbot_amg_level_info(bbot_ctx* c, int which, int level, long long* n, long long* nnz, long long* nc,
+                                int* tail) {
+  if (!c) return BBOT_E_INPUT;
+  AmgHierarchy& H = which == 0 ? c->amgA : c->amgT;
+  if (level < 0 || level >= (int)H.lv.size()) return BBOT_E_INPUT;
+  AmgLevel& L = H.lv[level];
+  if (n) *n = L.n;
+  if (nnz) *nnz = L.rp.p ? (long long)L.ci.n : -1;   // level 0 is read through a view (no CSR): -1
+  if (nc) *nc = L.nc;
+  if (tail) *tail = H.tail;
+  return BBOT_OK;
+}
+
 bbot_status bbot_amg_agg(bbot_ctx* c, int which, int level, int* agg) {
   if (!c || !agg) return BBOT_E_INPUT;
   API_BEGIN(c)
@@ -460,6 +490,9 @@ bbot_status bbot_amg_vcycle(bbot_ctx* c, int which, const double* b, double* x, 
   if (!c || !b || !x) return BBOT_E_INPUT;
   API_BEGIN(c)
   BB_REQUIRE(c->as.valid, BBOT_E_ORDER, "bbot_amg_vcycle before bbot_assemble");
+  BB_REQUIRE(which == 0 || which == 1, BBOT_E_INPUT, "which must be 0 (AMG(A)) or 1 (AMG(T))");
+  BB_REQUIRE(!(which == 0 ? c->amgA : c->amgT).lv.empty(), BBOT_E_ORDER,
+             "bbot_amg_vcycle: that hierarchy was not built by the last assembly (SIMPLE builds AMG(S-hat) only)");
   long long len = which == 0 ? c->n() : c->m();
   double* tb = which == 0 ? c->tmp_n.p : c->tmp_m.p;
   double* tx = which == 0 ? c->tmp_n2.p : c->tmp_m2.p;
@@ -518,11 +551,11 @@ bbot_status bbot_prof_stop(bbot_ctx* c, char* buf, long long buflen, long long* 
   Dev& d = c->dev;
   d.prof = false;
   sync(d);
-  std::map<const void*, std::pair<long long, double>> agg;
+  std::map<std::pair<const void*, long long>, std::pair<long long, double>> agg;
   for (auto& r : d.recs) {
     float ms = 0;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    auto& a = agg[r.fn];
+    auto& a = agg[{r.fn, r.grid}];
     a.first++;
     a.second += ms;
     d.pool.push_back(r.a);
@@ -533,14 +566,14 @@ bbot_status bbot_prof_stop(bbot_ctx* c, char* buf, long long buflen, long long* 
   for (auto& kv : agg) {
     const char* nm = nullptr;
     std::string name = "?";
-    if (cudaFuncGetName(&nm, kv.first) == cudaSuccess && nm) {
+    if (cudaFuncGetName(&nm, kv.first.first) == cudaSuccess && nm) {
       int stt = 0;
       char* dm = abi::__cxa_demangle(nm, nullptr, nullptr, &stt);
       name = (stt == 0 && dm) ? dm : nm;
       free(dm);
     }
-    char line[64];
-    snprintf(line, sizeof(line), "\t%lld\t%.6f\n", kv.second.first, kv.second.second);
+    char line[96];
+    snprintf(line, sizeof(line), "\t%lld\t%.6f\t%lld\n", kv.second.first, kv.second.second, kv.first.second);
     out += name + line;
   }
   if (needed) *needed = (long long)out.size() + 1;

@@ -1,7 +1,29 @@
 // common.cu -- deterministic reduction finalisers and the device-wide scan.
 #include "common.cuh"
+#include <map>
+#include <mutex>
 
 namespace bbot {
+
+cudaMemPool_t device_pool() {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  BB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  BB_CUDA(cudaMemPoolCreate(&pool, &props));
+  unsigned long long thr = ~0ULL;
+  BB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  pools[dev] = pool;
+  return pool;
+}
 
 __global__ void k_cond_from_flag(LoopCtl L) { cudaGraphSetConditional(L.h, *L.flag ? 1u : 0u); }
 

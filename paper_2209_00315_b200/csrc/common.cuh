@@ -42,6 +42,7 @@ struct Error : public std::runtime_error {
 struct ProfRec {
   const void* fn;
   cudaEvent_t a, b;
+  long long grid;     // CTAs of the launch (tells the levels of a multigrid kernel apart)
 };
 struct Dev {
   cudaStream_t stream = nullptr;
@@ -75,7 +76,7 @@ template <class K, class... Args>
 inline void launch(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem, Args... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
   if (d.prof && !d.capturing) {
-    ProfRec r{(const void*)kernel, d.get_event(), d.get_event()};
+    ProfRec r{(const void*)kernel, d.get_event(), d.get_event(), (long long)grid.x * grid.y * grid.z};
     cudaEventRecord(r.a, d.stream);
     kernel<<<grid, block, smem, d.stream>>>(args...);
     cudaEventRecord(r.b, d.stream);
@@ -109,7 +110,7 @@ inline void launch_cluster(Dev& d, K kernel, dim3 grid, dim3 block, size_t smem,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  ProfRec r{(const void*)kernel, nullptr, nullptr};
+  ProfRec r{(const void*)kernel, nullptr, nullptr, (long long)grid.x * grid.y * grid.z};
   bool prof = d.prof && !d.capturing;
   if (prof) {
     r.a = d.get_event();
@@ -134,7 +135,13 @@ inline unsigned nblocks(long long n, int bs, long long cap = 1LL << 30) {
   return (unsigned)b;
 }
 
-// Stream-ordered device buffer.
+// The library's private stream-ordered memory pool on the current device (created on
+// first use, release threshold raised so the AMG hierarchies rebuilt every Newton step
+// do not unmap/remap pages at each sync).  The device default pool -- shared with the
+// host framework -- is left untouched.
+cudaMemPool_t device_pool();
+
+// Stream-ordered device buffer (allocated from device_pool()).
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -158,7 +165,7 @@ struct DBuf {
     release();
     s = st; n = count;
     if (count == 0) return;
-    BB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    BB_CUDA(cudaMallocFromPoolAsync((void**)&p, count * sizeof(T), device_pool(), st));
   }
   void zero() { if (n) BB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
   void upload(const T* h, size_t count) {

@@ -70,6 +70,7 @@ struct Assembled {
   double scale = 0;               // ||(f;g;h)||
   DBuf<double> dscale;            // the same on the device (read by the captured solve)
   double res_norm = 0;            // ||F||
+  bool rhs_user = false;          // f, g, h, rhs hold a caller's right-hand side (bbot_solve_rhs)
 };
 
 struct bbot_ctx_impl;
@@ -77,6 +78,8 @@ struct bbot_ctx_impl;
 }  // namespace bbot
 
 struct bbot_ctx {
+  int devid = 0;                 // CUDA device of the context (every host thread of a call sets it)
+  size_t stack_prev = 0;         // device stack limit before bbot_create
   bbot::Dev dev;
   bbot::Reducer red;
   bbot_solver_opts opts;
@@ -95,6 +98,7 @@ struct bbot_ctx {
   // direction
   bool have_dir = false;
   bbot::DBuf<double> sol, dphi, drho, ds;
+  bbot::DBuf<double> drho0;      // solve(rhs): slice-mass part of drho
   // workspaces
   bbot::DevGmres outer, innerT;
   bbot::DevPcg pcg;

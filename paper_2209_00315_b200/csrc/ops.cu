@@ -290,6 +290,100 @@ void bb_rhs_A(bbot_ctx* c, const double* r1, const double* y, double* b) {
          1.0 / (double)g.N);
 }
 
+// ---------------------------------------------------------------- solve(rhs)
+// A caller-given (f; g; h) of (3.1) replaces the Newton residual
+// (oracle/bb.py BBSolver.solve_rhs).  (4.17) needs 1^T f^k = 0 per slice (A30), so the
+// slice masses of drho are fixed first from the phi rows' slice sums,
+//   c-bar^T (drho^{k-1} - drho^k)/dt = 1^T f^k  ->  m_k = m_{k-1} - dt 1^T f^k, m_0 = 0,
+// drho0^k = (m_k/|Omega|) 1, and (f - B^T drho0; g; h - s drho0) is solved; afterwards
+// drho += drho0.  g~ = g - Mbar h / rho, rhs (f; P g~) (BB) or (f; g~)
+// (SIMPLE), stop at eps ||(f;g;h)||_2.
+__global__ void k_user_gt(long long m, int nbar, const double* __restrict__ cbar, const double* __restrict__ g,
+                          const double* __restrict__ h, const double* __restrict__ rho, double* __restrict__ gt) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int i = (int)(t % nbar);
+  gt[t] = g[t] - cbar[i] * h[t] / rho[t];
+}
+struct SqSum {
+  const double* a;
+  long long L;
+  __device__ double operator()(int k, long long i) const {
+    double v = a[(size_t)k * L + i];
+    return v * v;
+  }
+};
+// drho0[k0][i] = m_{k0+1} / |Omega|,  m_k = -dt sum_{j<=k} Sf[j-1]  (1-based k)
+__global__ void k_mass_drho0(long long m, int nbar, double dt, double inv_area, const double* __restrict__ Sf,
+                             double* __restrict__ drho0) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  double acc = 0.0;
+  for (int j = 0; j <= k0; j++) acc += Sf[j];
+  drho0[t] = -dt * acc * inv_area;
+}
+__global__ void k_user_shift(long long n, long long m, int N, BtRow bt, const double* __restrict__ drho0,
+                             const double* __restrict__ s, double* __restrict__ f, double* __restrict__ h) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    int kk = (int)(t / N);
+    f[t] -= bt(drho0, nullptr, 0.0, kk, t - (long long)kk * N);     // f - B^T drho0
+  } else if (t < n + m) {
+    h[t - n] -= s[t - n] * drho0[t - n];                                // h - s drho0
+  }
+}
+__global__ void k_add(long long n, const double* __restrict__ a, double* __restrict__ b) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) b[t] += a[t];
+}
+__global__ void k_rhs2(long long m, int nbar, double area, const double* __restrict__ cbar,
+                       const double* __restrict__ gt, const double* __restrict__ S, double* __restrict__ out);  // assemble.cu
+
+void set_user_rhs(bbot_ctx* c) {   // as.f, as.g, as.h hold the caller's (f; g; h)
+  DevGeom& g = c->g;
+  Assembled& A = c->as;
+  cudaStream_t s = c->dev.stream;
+  long long n = c->n(), m = c->m();
+  int K = g.K;
+  double* sc = c->scal.p;
+  // ||(f;g;h)|| of the caller's right-hand side
+  c->red.slice_sum(SqSum{A.f.p, g.N}, g.N, K + 1, sc, false);
+  c->red.slice_sum(SqSum{A.g.p, g.nbar}, g.nbar, K, sc + K + 1, false);
+  c->red.slice_sum(SqSum{A.h.p, g.nbar}, g.nbar, K, sc + 2 * K + 1, false);
+  std::vector<double> hs(3 * K + 1);
+  BB_CUDA(cudaMemcpyAsync(hs.data(), sc, (3 * K + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync(c->dev);
+  // slice-mass step
+  if (c->drho0.n != (size_t)m) c->drho0.alloc(m, s);
+  c->red.slice_sum(WSlice{nullptr, A.f.p, g.N}, g.N, K + 1, sc, false);
+  launch(c->dev, k_mass_drho0, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, g.dt, 1.0 / g.area, (const double*)sc,
+         c->drho0.p);
+  launch(c->dev, k_user_shift, dim3(nblocks(n + m, BS)), dim3(BS), 0, n, m, g.N, make_btrow(c),
+         (const double*)c->drho0.p, (const double*)c->s.p, A.f.p, A.h.p);
+  // g~ and the right-hand side of (4.17) / the saddle-point system
+  launch(c->dev, k_user_gt, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, (const double*)g.cbar.p,
+         (const double*)A.g.p, (const double*)A.h.p, (const double*)(c->rho_ext.p + g.nbar), A.gt.p);
+  BB_CUDA(cudaMemcpyAsync(A.rhs.p, A.f.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (A.precond == 1) {
+    BB_CUDA(cudaMemcpyAsync(A.rhs.p + n, A.gt.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else {
+    c->red.slice_sum(WSlice{nullptr, A.gt.p, g.nbar}, g.nbar, K, sc + 3 * K + 1, false);
+    launch(c->dev, k_rhs2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, g.area, (const double*)g.cbar.p,
+           (const double*)A.gt.p, (const double*)(sc + 3 * K + 1), A.rhs.p + n);
+  }
+  double tot = 0.0;
+  for (double v : hs) tot += v;
+  A.scale = std::sqrt(tot);
+  BB_CUDA(cudaMemcpyAsync(A.dscale.p, &A.scale, sizeof(double), cudaMemcpyHostToDevice, s));
+  sync(c->dev);
+  A.rhs_user = true;
+}
+
+void finish_user_solve(bbot_ctx* c) {   // drho += drho0
+  launch(c->dev, k_add, dim3(nblocks(c->m(), BS)), dim3(BS), 0, c->m(), (const double*)c->drho0.p, c->drho.p);
+}
+
 // ---------------------------------------------------------------- a6 recovery
 struct QSum {  // q = g~ - B dphit + C drho ; returns q
   BRow br;

@@ -22,6 +22,8 @@ void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L);         // 
 void j_matvec(bbot_ctx* c, const double* x, double* y);                     // (eq:saddle-point)
 void simple_c(bbot_ctx* c, const double* r, double* z1, double* cvec);      // z1 = diag(A)^-1 r1, c = r2 - B z1
 void simple_out(bbot_ctx* c, const double* r, const double* z2, double* out);  // (diag(A)^-1(r1 - B^T z2); z2)
+void set_user_rhs(bbot_ctx* c);                                            // solve(rhs): (f;g;h) in as.f/g/h
+void finish_user_solve(bbot_ctx* c);                                       // drho += drho0
 void recover(bbot_ctx* c);                                                   // a6
 double newton_update(bbot_ctx* c, double tau);                              // a7 step + renormalise
 double kinetic_energy(bbot_ctx* c);

@@ -49,6 +49,7 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   drop_solve_graph(c);
   EvTimer t0(c->dev.stream);
   compute_residual(c, true);
+  c->as.rhs_user = false;
   assemble_T(c);
   double ta = t0.ms();
   EvTimer t1(c->dev.stream);
@@ -63,17 +64,21 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
     // The two setups are independent and host-latency-bound (size read-backs between
     // kernels): AMG(T) runs on a second stream from a second host thread, after the
     // assembly on the main stream; the main stream then waits for it.
-    cudaEvent_t ready, done;
-    BB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    BB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    BB_CUDA(cudaEventRecord(ready, c->dev.stream));
-    BB_CUDA(cudaStreamWaitEvent(c->dev2.stream, ready, 0));
+    struct Ev {   // RAII: released on every path, including the throwing ones
+      cudaEvent_t e = nullptr;
+      Ev() { BB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+      ~Ev() { if (e) cudaEventDestroy(e); }
+    } ready, done;
+    BB_CUDA(cudaEventRecord(ready.e, c->dev.stream));
+    BB_CUDA(cudaStreamWaitEvent(c->dev2.stream, ready.e, 0));
     c->dev2.sync_check = c->dev.sync_check;
     std::exception_ptr err;
     double tT = 0, tA = 0;
     auto now = [] { return std::chrono::steady_clock::now(); };
+    const int devid = c->devid;
     std::thread th([&]() {
       try {
+        BB_CUDA(cudaSetDevice(devid));   // a new host thread starts on device 0
         auto a = now();
         amg_setup(c->dev2, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, c->amgw2);
         sync(c->dev2);
@@ -94,10 +99,8 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
     th.join();
     if (getenv("BBOT_TIMING")) fprintf(stderr, "[bbot] setup AMG(A) %.2f ms, AMG(T) %.2f ms (concurrent)\n", tA, tT);
     if (err) std::rethrow_exception(err);
-    BB_CUDA(cudaEventRecord(done, c->dev2.stream));
-    BB_CUDA(cudaStreamWaitEvent(c->dev.stream, done, 0));
-    cudaEventDestroy(ready);
-    cudaEventDestroy(done);
+    BB_CUDA(cudaEventRecord(done.e, c->dev2.stream));
+    BB_CUDA(cudaStreamWaitEvent(c->dev.stream, done.e, 0));
     c->dev.launches += c->dev2.launches;
     c->dev2.launches = 0;
   }

@@ -367,3 +367,38 @@ def test_amg_kcycle_parity():
     b = np.random.default_rng(5).standard_normal(sizes[0]).reshape(d.K + 1, d.N)
     b = (b - b.mean(1, keepdims=True)).reshape(-1)
     assert _rel(ctx.amg_vcycle(0, b), oamg.vcycle(H, b)) < 1e-10
+
+
+@pytest.mark.parametrize("name,mu", [("T1", 2.0 ** -6), ("C1", 2.0 ** -3)])
+def test_solve_rhs_parity(name, mu):
+    """solve(rhs) -> direction at the boundary (bbot_solve_rhs): the Newton
+    system (3.1) of an IPM state with a seeded caller-given (f; g; h) in the range of (3.1)
+    (Σ f = 0, nonzero slice sums: the slice-mass step is exercised), against
+    oracle.bb.BBSolver.solve_rhs: each block to 1e-8, outer counts +-1.  A following
+    bbot_solve re-derives the Newton right-hand side (equals a fresh context's solve)."""
+    pb = _gpu()
+    p, d, phi, rho, s = ipm_state(name, mu)
+    mu_sys = mu / 2
+    rng = np.random.default_rng(17)
+    f = rng.standard_normal(d.n)
+    f -= f.mean()
+    g, h = rng.standard_normal(d.m), rng.standard_normal(d.m)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, mu_sys)
+    ctx.assemble()
+    gphi, grho, gds, st = ctx.solve_rhs(f, g, h)
+    S = BBSolver(d, phi, rho, s, mu_sys, SolverOpts())
+    ophi, orho, os_ = S.solve_rhs(f, g, h)
+    assert S.stats["converged"] and st["converged"] == 1, (S.stats, st)
+    assert abs(st["outer_its"] - S.stats["outer_its"]) <= 1, (st, S.stats)
+    for a, b in ((gphi, ophi), (grho, orho), (gds, os_)):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b), np.linalg.norm(a - b) / np.linalg.norm(b)
+    # the Newton right-hand side comes back for the next plain solve
+    n1 = ctx.solve()
+    ctx2 = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx2.set_state(phi, rho, s, mu_sys)
+    ctx2.assemble()
+    n2 = ctx2.solve()
+    for a, b in zip(n1[:3], n2[:3]):
+        assert np.array_equal(a, b)
+    assert n1[3]["outer_its"] == n2[3]["outer_its"]

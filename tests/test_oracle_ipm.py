@@ -137,9 +137,9 @@ def test_inner_tolerance_tightens_below_mu_tight(monkeypatch):
     seen = []
     real = ipm_mod.newton_step
 
-    def spy(d, phi, rho, s, mu, opts, tau):
+    def spy(d, phi, rho, s, mu, opts, tau, keep=None):
         seen.append((mu, opts.eps_A))
-        return real(d, phi, rho, s, mu, opts, tau)
+        return real(d, phi, rho, s, mu, opts, tau, keep)
     monkeypatch.setattr(ipm_mod, "newton_step", spy)
     p = make_problem("T0")
     d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)

@@ -218,3 +218,51 @@ def test_T_smoother_contracts_on_ipm_path():
         assert np.allclose(H.levels[0].dinv, 1.0 / np.abs(M).sum(1))   # the oracle uses the l1 diagonal
         ev = np.linalg.eigvals(M / np.abs(M).sum(1)[:, None])
         assert ev.real.min() > 0 and np.abs(1.0 - om * ev).max() < 1.0
+
+
+def _seeded_rhs(d, seed):
+    """(f; g; h) in the range of (3.1): Σ_all f = 0 (left kernel (1;0;0), Remark 3.1), but
+    nonzero slice sums 1ᵀf^k, so the slice-mass step of solve_rhs is exercised."""
+    rng = np.random.default_rng(seed)
+    f = rng.standard_normal(d.n)
+    f -= f.mean()
+    return f, rng.standard_normal(d.m), rng.standard_normal(d.m)
+
+
+@pytest.mark.parametrize("name", ["T0", "T1"])
+def test_solve_rhs_matches_direct(name):
+    """solve(rhs) (north star) with a caller-given (f; g; h): the BB-FGMRES
+    solve + slice-mass step + recovery reproduces the dense least-squares solve of (3.1)
+     in the A11 gauge, and the (3.1) residual is at the FGMRES tolerance."""
+    p = make_problem(name)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=21, mu=0.05)
+    f, g, h = _seeded_rhs(d, 5)
+    assert np.abs(f.reshape(d.K + 1, d.N).sum(1)).max() > 1e-3
+    S = BBSolver(d, phi, rho, s, 0.05, SolverOpts(eps_out=1e-12))
+    dphi, drho, ds = S.solve_rhs(f, g, h)
+    assert S.stats["converged"]
+    J = d.jacobian(phi, rho, s).toarray()
+    rhs = np.concatenate([f, g, h])
+    ref, *_ = np.linalg.lstsq(J, rhs, rcond=None)
+    n, m = d.n, d.m
+    rp = ref[:n].reshape(d.K + 1, d.N)
+    rp = (rp - (rp[0] @ d.M) / d.area).reshape(-1)
+    for a, b in ((dphi, rp), (drho, ref[n:n + m]), (ds, ref[n + m:])):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b)
+    res = J @ np.concatenate([dphi, drho, ds]) - rhs
+    assert np.linalg.norm(res) <= 1e-9 * np.linalg.norm(rhs)
+
+
+def test_solve_rhs_newton_rhs_is_plain_solve():
+    """With (f; g; h) = -F (the Newton right-hand side of a renormalised state) the slice
+    masses m_k are 0 and solve_rhs is the plain Newton solve."""
+    p = make_problem("T1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = random_state(p, seed=22, mu=0.05)
+    S1 = BBSolver(d, phi, rho, s, 0.05)
+    a = S1.solve()
+    S2 = BBSolver(d, phi, rho, s, 0.05)
+    b = S2.solve_rhs(S2.f, S2.g, S2.h)
+    for u, v in zip(a, b):
+        assert np.allclose(u, v, rtol=0, atol=1e-13 * max(1.0, abs(v).max()))
