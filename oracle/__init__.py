@@ -19,6 +19,7 @@ line n; S:n = SPEC.md line n; A-numbers are the readings of SURVEY.md §8(c)
   krylov.py  I1,I4,I5  FGMRES, per-slice PCG, GMRES(10)
   bb.py      I2, a6 BB preconditioner apply (4.18)-(4.20)+(4.26), recovery (4.15)
   simple.py  f1     SIMPLE preconditioner on (eq:saddle-point), NEXT row
+  hss.py     f2     HSS preconditioner (eq:prec-hss), NEXT row
   ipm.py     a7     interior-point loop
   direct.py         dense direct solve of (3.1) for tiny instances (pin)
 

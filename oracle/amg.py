@@ -30,7 +30,10 @@ Definition (both sides):
     <= coarse_max (1024); or no coarsening (n_c > 0.9 n); or max_levels.
   * smoother: damped Jacobi (omega), V(1,1) from a zero initial guess.
   * coarsest: mode "A": per slice, grounded at the slice's first row, then the
-    slice mean removed;  mode "T": dense solve.
+    slice mean removed;  mode "T": dense solve;  mode "As" (the shifted, nonsingular
+    per-slice blocks A_k + alpha I of the HSS preconditioner, NEXT f2): everything as
+    mode "A" except that the per-slice coarsest block is inverted as it is (no grounding,
+    no mean removal).
 """
 from __future__ import annotations
 
@@ -169,9 +172,10 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
     while True:
         n = cur.shape[0]
         dg = (np.asarray(abs(cur).sum(axis=1)).ravel() if mode == "T" else cur.diagonal())
+        perslice = mode in ("A", "As")
         lv = Level(A=cur, slice_of_row=cur_slice, dinv=1.0 / dg)
         levels.append(lv)
-        small = (_slice_sizes(cur_slice, nslices).max() <= coarse_max) if mode == "A" else (n <= coarse_max)
+        small = (_slice_sizes(cur_slice, nslices).max() <= coarse_max) if perslice else (n <= coarse_max)
         if small or len(levels) >= max_levels:
             break
         agg1, nc1, sl1 = match(cur, cur_slice)
@@ -185,9 +189,9 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
         cur_slice = sl2
     H = Hierarchy(levels=levels, mode=mode, omega=omega, nslices=nslices)
     L = len(levels)
-    H.kcycle = [mode == "A" and L >= KC_MIN_LEVELS and 0 < l < L - 1 and
+    H.kcycle = [mode in ("A", "As") and L >= KC_MIN_LEVELS and 0 < l < L - 1 and
                 _slice_sizes(levels[l].slice_of_row, nslices).max() <= KC_ROWS for l in range(L)]
-    Ac = levels[-1].A.toarray() if (mode == "A" or levels[-1].A.shape[0] <= coarse_max) else None
+    Ac = levels[-1].A.toarray() if (mode in ("A", "As") or levels[-1].A.shape[0] <= coarse_max) else None
     if mode == "A":
         sl = levels[-1].slice_of_row
         for k in range(nslices):
@@ -195,6 +199,11 @@ def setup(A: sp.csr_matrix, slice_of_row: np.ndarray, mode: str, omega: float,
             blk = Ac[np.ix_(rows, rows)]
             inv = np.linalg.inv(blk[1:, 1:]) if rows.size > 1 else np.zeros((0, 0))
             H.coarse_inv.append((rows, inv))
+    elif mode == "As":
+        sl = levels[-1].slice_of_row
+        for k in range(nslices):
+            rows = np.nonzero(sl == k)[0]
+            H.coarse_inv.append((rows, np.linalg.inv(Ac[np.ix_(rows, rows)])))
     elif Ac is not None:
         H.coarse_dense_inv = np.linalg.inv(Ac)
     # else: coarsening stalled above coarse_max (decoupled rows: e.g. AMG(Ŝ) at φ = 0 collapses
@@ -209,6 +218,10 @@ def _coarse_solve(H: Hierarchy, b):
             return H.omega * H.levels[-1].dinv * b
         return H.coarse_dense_inv @ b
     x = np.zeros_like(b)
+    if H.mode == "As":                          # nonsingular blocks: plain per-slice solve
+        for rows, inv in H.coarse_inv:
+            x[rows] = inv @ b[rows]
+        return x
     for rows, inv in H.coarse_inv:
         if rows.size == 0:
             continue

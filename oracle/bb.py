@@ -38,8 +38,10 @@ class SolverOpts:
     coarse_max_A: int = 64        # rows per slice
     coarse_max_T: int = 1024      # rows in total
     exact_inner: bool = False     # pin mode: exact T solve + exact A_k^+ (no AMG)
-    precond: str = "bb"           # "bb" (§4.5) or "simple" (§5.3, NEXT row f1)
-    coarse_max_S: int = 256       # AMG(Ŝ) coarsest rows (SIMPLE, A32)
+    precond: str = "bb"           # "bb" (§4.5), "simple" (§5.3, NEXT f1) or "hss" (§5.1, NEXT f2)
+    coarse_max_S: int = 256       # AMG(Ŝ) coarsest rows (SIMPLE, A32; also HSS's K-solve)
+    alpha_hss: float = 0.5        # HSS relaxation parameter α
+    eps_in_hss: float = 1e-1      # HSS inner tolerance ε_in
 
 
 class BBSolver:

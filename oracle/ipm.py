@@ -19,6 +19,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from .bb import BBSolver, SolverOpts
+from .hss import HssSolver
 from .simple import SimpleSolver
 from .ops import Discretisation
 
@@ -61,7 +62,7 @@ def res_norm(d, phi, rho, s, mu):
 
 
 def newton_step(d: Discretisation, phi, rho, s, mu, opts: SolverOpts, tau: float, keep=None):
-    S = (SimpleSolver if opts.precond == "simple" else BBSolver)(d, phi, rho, s, mu, opts)
+    S = {"simple": SimpleSolver, "hss": HssSolver}.get(opts.precond, BBSolver)(d, phi, rho, s, mu, opts)
     dphi, drho, ds = S.solve()
     if keep is not None:            # test hook: the system solved and its direction
         keep.update(state=(phi, rho, s), mu=mu, opts=opts, direction=(dphi, drho, ds))
