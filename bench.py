@@ -292,7 +292,7 @@ def ncu_traffic(config, kernel):
         short = kernel.replace("void ", "").replace("bbot::", "")
         for k, v in per.items():
             if k.replace("void ", "").replace("bbot::", "") == short:
-                return v, summ.get("round", {}).get(config, "r1")
+                return v, summ.get("round", {}).get(f"{config}/{k}", "r1")
     except Exception:
         pass
     return None, None

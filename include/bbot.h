@@ -63,12 +63,19 @@ typedef struct {
   double omega_T;      /* l1-Jacobi weight, AMG(T) [1.0] (D = sum_j |T_ij|, I3)             */
   int coarse_max_A;    /* AMG(A) coarsest: max rows per time slice [64]                     */
   int coarse_max_T;    /* AMG(T) coarsest: max rows in total [1024]                         */
-  int precond;         /* 0 = BB on (4.17) [0]; 1 = SIMPLE on the saddle-point system
+  int precond;         /* 0 = BB on (4.17) [0]; 2 = HSS (below); 1 = SIMPLE on the saddle-point system
                         * (eq:saddle-point) with eq:sca-precs: FGMRES
                         * on J = [[A, B^T],[B, -C]], rhs (f; g~); the inner solve is
                         * S-hat = C + B diag(A)^-1 B^T (stored in T's slot, A31/A32) by
                         * GMRES(restart_T) + AMG, eps_T; recovery dphi = x1, drho = x2.   */
   int coarse_max_S;    /* AMG(S-hat) coarsest: max rows in total [256] (A32)                 */
+  /* precond = 2: HSS (NEXT f2, eq:prec-hss) on the same saddle-point system as
+   * SIMPLE, diagonally scaled: M^-1 = D^-1/2 H_a^-1 K_a^-1 D^-1/2 diag(I,-I),
+   * D = diag(diag(A), C); K_a^-1 by the dual Schur complement a I + B^ B^T/a (eq:solve-K,
+   * stored in T's slot, GMRES(restart_T) + AMG), H_a^-1 by per-slice PCG + AMG on the scaled
+   * shifted Laplacians A^_k + a I (eq:solve-laplacians); both inner solves to eps_in_hss. */
+  double alpha_hss;    /* HSS relaxation parameter [0.5]                              */
+  double eps_in_hss;   /* HSS inner tolerance [1e-1]                                  */
 } bbot_solver_opts;
 
 typedef struct {

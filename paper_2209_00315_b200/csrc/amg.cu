@@ -414,11 +414,12 @@ __global__ void k_up_dot(V v, const double* __restrict__ dinv, const double* __r
 // ------------------------------------------------------------ coarsest
 // mode A: per slice, grounded at the slice's first row; Gauss-Jordan with partial
 // pivoting on [B | I] in shared memory, B = block without row/col 0.
-__global__ void k_coarseA_setup(const long long* __restrict__ sptr, CsrView A, int cm, double* cinv) {
+// grounded = 0 (mode As): the whole block is inverted (nonsingular shifted Laplacian).
+__global__ void k_coarseA_setup(const long long* __restrict__ sptr, CsrView A, int cm, double* cinv, int grounded) {
   extern __shared__ double sm[];
   int k = blockIdx.x;
-  long long s0 = sptr[k];
-  int nl = (int)(sptr[k + 1] - s0) - 1;   // grounded size
+  long long s0 = sptr[k] + (grounded ? 1 : 0) - 1;   // first row of the block is s0 + 1
+  int nl = (int)(sptr[k + 1] - sptr[k]) - (grounded ? 1 : 0);
   if (nl <= 0) return;
   int w = 2 * nl;
   double* M = sm;                          // nl x 2nl
@@ -471,13 +472,21 @@ __global__ void k_coarseA_setup(const long long* __restrict__ sptr, CsrView A, i
 }
 
 __global__ void k_coarseA_apply(const long long* __restrict__ sptr, int cm, const double* __restrict__ cinv,
-                                const double* __restrict__ b, double* x) {
+                                const double* __restrict__ b, double* x, int grounded) {
   __shared__ double xs[256];
   int k = blockIdx.x;
   long long s0 = sptr[k];
   int nloc = (int)(sptr[k + 1] - s0);
   if (nloc <= 0) return;
   const double* inv = cinv + (size_t)k * cm * cm;
+  if (!grounded) {                 // mode As: x = inv b on the slice block
+    for (int j = threadIdx.x; j < nloc; j += blockDim.x) {
+      double acc = 0.0;
+      for (int l = 0; l < nloc; l++) acc += inv[j * cm + l] * b[s0 + l];
+      x[s0 + j] = acc;
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < nloc; j += blockDim.x) {
     double acc = 0.0;
     if (j > 0)
@@ -534,6 +543,7 @@ struct TailArgs {
   int first, last;             // levels first..last (last = coarsest)
   double om;
   int cm;
+  int grounded;                // 1: mode A (grounded + mean removed), 0: mode As (plain)
   const double* cinv;
   // restriction into level `first` from level first-1
   const long long* mptr0;
@@ -618,6 +628,16 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
     long long s0 = C.sptr[P.k];
     int nloc = (int)(C.sptr[P.k + 1] - s0);
     const double* inv = T->cinv + (size_t)P.k * T->cm * T->cm;
+    if (!T->grounded) {                         // mode As: nonsingular block, plain solve
+      if (P.c == 0)
+        for (int j = tid; j < nloc; j += bs) {
+          double acc = 0.0;
+          for (int l = 0; l < nloc; l++) acc += inv[j * T->cm + l] * C.b[s0 + l];
+          C.xo[s0 + j] = acc;
+        }
+      tail_sync();
+      return;
+    }
     for (int j = tid; j < nloc; j += bs) {      // every CTA of the cluster computes it (tiny)
       double acc = 0.0;
       if (j > 0)
@@ -1105,7 +1125,7 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     std::vector<long long>& sp = H.lv[l].sptr;
     long long maxs = 0;
     for (int k = 0; k < nslices; k++) maxs = std::max(maxs, sp[k + 1] - sp[k]);
-    bool small = (mode == 0) ? (maxs <= coarse_max) : (n <= coarse_max);
+    bool small = (mode != 1) ? (maxs <= coarse_max) : (n <= coarse_max);
     if (small || l + 1 >= MAX_LEVELS) break;
     // pass 1 on level l
     DBuf<int> agg1, sl1, agg2, sl2;
@@ -1154,18 +1174,20 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     C.v.alloc(std::max(1LL, nnz), s);
     launch(d, k_view_fill<V0>, dim3(nblocks(n, BS)), dim3(BS), 0, v0, (const long long*)C.rp.p, C.ci.p, C.v.p);
   }
-  if (mode == 0) {
+  if (mode != 1) {
+    const int grounded = mode == 0 ? 1 : 0;
     long long maxs = 0;
     for (int k = 0; k < nslices; k++) maxs = std::max(maxs, C.sptr[k + 1] - C.sptr[k]);
-    BB_REQUIRE(maxs <= 121, BBOT_E_INTERNAL, "AMG(A): coarsest slice block too large");
-    H.cm = (int)std::max(1LL, maxs - 1);
+    BB_REQUIRE(maxs - grounded <= 120, BBOT_E_INTERNAL, "AMG(A): coarsest slice block too large");
+    H.cm = (int)std::max(1LL, maxs - grounded);
     H.cinv.alloc((size_t)nslices * H.cm * H.cm, s);
     H.cinv.zero();
     H.csptr.alloc(nslices + 1, s);
     BB_CUDA(cudaMemcpyAsync(H.csptr.p, C.sptr.data(), (nslices + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
     size_t smem = (size_t)H.cm * 2 * H.cm * sizeof(double);
     BB_CUDA(cudaFuncSetAttribute(k_coarseA_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch(d, k_coarseA_setup, dim3(nslices), dim3(256), smem, (const long long*)H.csptr.p, C.view(), H.cm, H.cinv.p);
+    launch(d, k_coarseA_setup, dim3(nslices), dim3(256), smem, (const long long*)H.csptr.p, C.view(), H.cm, H.cinv.p,
+           grounded);
   } else if (C.n > coarse_max) {   // stalled coarsening: Jacobi coarsest (oracle/amg.py)
     H.cjac = true;
     H.cm = (int)C.n;
@@ -1256,8 +1278,8 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
     fprintf(stderr, "[bbot]   amg mode %d coarsest (%lld rows) + SELL: %.2f ms\n", mode, H.lv.back().n,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lv).count());
   }
-  if (mode == 0) H.tail = 0;
-  if (mode == 0 && H.lv.size() >= 2) {
+  if (mode != 1) H.tail = 0;
+  if (mode != 1 && H.lv.size() >= 2) {
     int L = (int)H.lv.size();
     long long lim = L >= KC_MIN_LEVELS ? (long long)KC_ROWS : TAIL_ROWS;
     for (int l = 1; l < L && lim > 0; l++) {
@@ -1291,9 +1313,9 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
 
 static void coarse_solve(Dev& d, AmgHierarchy& H, const double* b, double* x) {
   AmgLevel& C = H.lv.back();
-  if (H.mode == 0)
+  if (H.mode != 1)
     launch(d, k_coarseA_apply, dim3(H.nslices), dim3(128), 0, (const long long*)H.csptr.p, H.cm,
-           (const double*)H.cinv.p, b, x);
+           (const double*)H.cinv.p, b, x, H.mode == 0 ? 1 : 0);
   else if (H.cjac)
     launch(d, k_jacobi0, dim3(nblocks(C.n, 256)), dim3(256), 0, C.n, (const double*)C.dinv.p, b, H.omega, x);
   else
@@ -1312,6 +1334,7 @@ static void tail_args(AmgHierarchy& H, TailArgs& T) {
   T.last = L - 1;
   T.om = H.omega;
   T.cm = H.cm;
+  T.grounded = H.mode == 0 ? 1 : 0;
   T.cinv = H.cinv.p;
   AmgLevel& P = H.lv[H.tail - 1];
   T.mptr0 = P.mptr.p;
@@ -1345,7 +1368,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
   int L = (int)H.lv.size();
   if (L == 1) { coarse_solve(d, H, b, x); return false; }
   double om = H.omega;
-  if (H.mode != 0) active = nullptr;                // T couples slices: never skip
+  if (H.mode == 1) active = nullptr;                // T couples slices: never skip
   const long long L0 = H.lv[0].n / std::max(1, H.nslices);
   auto skip_at = [&](int l) { return SliceSkip{active, l == 0 ? nullptr : (const int*)H.lv[l].slice_of.p, L0}; };
   // grid-wide levels: 0 .. stop-1; below: the per-slice tail (mode A) or more grid levels
@@ -1365,7 +1388,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
       launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
              (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1));
   }
-  if (H.mode == 0 && H.tail > 0) {
+  if (H.mode != 1 && H.tail > 0) {
     int cl = TAIL_CL > 0 ? std::min(TAIL_CL, TAIL_MAXCL)
                          : std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
     launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(TAIL_BS), 0, cl, (const TailArgs*)H.tail_args.p, active);
@@ -1408,6 +1431,10 @@ template void amg_setup<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, 
                                       AmgWork&);
 template bool amg_vcycle<LapView>(Dev&, AmgHierarchy&, const LapView&, const double*, double*,
                                   const SliceDotFuse*, const double*);
+template void amg_setup<ScaledLapView>(Dev&, AmgHierarchy&, const ScaledLapView&, const int*, int, int, double, int,
+                                       AmgWork&);
+template bool amg_vcycle<ScaledLapView>(Dev&, AmgHierarchy&, const ScaledLapView&, const double*, double*,
+                                        const SliceDotFuse*, const double*);
 template bool amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*,
                                        const SliceDotFuse*, const double*);
 

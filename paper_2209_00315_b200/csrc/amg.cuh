@@ -49,6 +49,37 @@ struct LapView {
   }
 };
 
+// HSS (NEXT f2): the diagonally scaled, shifted blocks
+//   Â_k + alpha I = D_A^{-1/2} A_k D_A^{-1/2} + alpha I,  sA = D_A^{-1/2} (per row),
+// read from the same cell-ELL storage as LapView (nothing extra is stored).
+struct ScaledLapView {
+  int N;
+  long long nrows;
+  const int* nb;        // [4][N]
+  const double* off;    // [K+1][4][N]
+  const double* sA;     // [n]
+  double alpha;
+  template <class F>
+  __device__ __forceinline__ void row(long long r, F&& f) const {
+    int kk = (int)(r / N);
+    int fc = (int)(r - (long long)kk * N);
+    const double* o = off + (size_t)kk * 4 * N + fc;
+    long long base = (long long)kk * N;
+    const double sr = sA[r];
+    double d = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      int c = nb[t * N + fc];
+      if (c >= 0) {
+        double a = o[(size_t)t * N];
+        d -= a;
+        f(base + c, a * sr * sA[base + c]);
+      }
+    }
+    f(r, d * sr * sr + alpha);
+  }
+};
+
 // rows r = k0*nbar + i; T values tv[((k0*3 + d)*W + s)*nbar + i], column
 // (k0+d-1)*nbar + tcol[s*nbar + i]; unused slots (tcol = -1) hold exactly 0 and
 // are read as column i (adds an exact 0; no data-dependent loop exit)
@@ -173,7 +204,8 @@ struct AmgLevel {
 };
 
 struct AmgHierarchy {
-  int mode = 0;            // 0 = A (per-slice grounded coarsest), 1 = T (dense coarsest)
+  int mode = 0;            // 0 = A (per-slice grounded coarsest), 1 = T (dense coarsest),
+                           // 2 = As (HSS shifted blocks: per slice, nonsingular coarsest)
   double omega = 0.7;
   int nslices = 0;
   std::vector<AmgLevel> lv;

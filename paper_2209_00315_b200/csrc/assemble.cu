@@ -203,6 +203,9 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
 }
 
 LapView view_A(bbot_ctx* c) { return LapView{c->g.N, c->n(), c->g.fadj_nb.p, c->as.Aoff.p}; }
+ScaledLapView view_As(bbot_ctx* c) {
+  return ScaledLapView{c->g.N, c->n(), c->g.fadj_nb.p, c->as.Aoff.p, c->as.sA.p, c->opts.alpha_hss};
+}
 SliceEllView view_T(bbot_ctx* c) {
   return SliceEllView{c->g.nbar, c->g.K, c->g.W, c->m(), c->g.tcol.p, c->as.Tv.p};
 }
@@ -390,7 +393,7 @@ void compute_residual(bbot_ctx* c, bool write_rhs) {
   if (write_rhs) {
     c->red.slice_sum(GtSum{g.nbar, A.gt.p}, g.nbar, K, sc + 2 * K + 1, false);
     BB_CUDA(cudaMemcpyAsync(A.rhs.p, A.f.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (c->opts.precond == 1)    // SIMPLE: the unprojected saddle-point system
+    if (c->opts.precond != 0)    // SIMPLE / HSS: the unprojected saddle-point system
       BB_CUDA(cudaMemcpyAsync(A.rhs.p + n, A.gt.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
     else
       launch(c->dev, k_rhs2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, g.area, (const double*)g.cbar.p,
@@ -536,21 +539,63 @@ __global__ void __launch_bounds__(128) k_assemble_S(
   }
 }
 
+// HSS (NEXT f2): sA = diag(A)^-1/2, sC = C^-1/2, c2 = alpha^2 C
+__global__ void k_hss_scal(long long n, long long m, double al, const double* __restrict__ dAinv,
+                           const double* __restrict__ Cd, double* __restrict__ sA, double* __restrict__ sC,
+                           double* __restrict__ c2) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) sA[t] = sqrt(dAinv[t]);
+  if (t < m) {
+    sC[t] = 1.0 / sqrt(Cd[t]);
+    c2[t] = al * al * Cd[t];
+  }
+}
+// T-slot values *= inv_alpha sC_row sC_col  (rows k0*nbar+i, column (k0+d-1)*nbar + tcol[s][i])
+__global__ void k_hss_scale_S(int nbar, int K, int W, double inv_alpha, const int* __restrict__ tcol,
+                              const double* __restrict__ sC, double* __restrict__ Tv) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)K * nbar) return;
+  int k0 = (int)(t / nbar), i = (int)(t - (long long)k0 * nbar);
+  const double sr = inv_alpha * sC[t];
+  for (int d = 0; d < 3; d++) {
+    int kk = k0 + d - 1;
+    if (kk < 0 || kk >= K) continue;
+    for (int s = 0; s < W; s++) {
+      int col = tcol[(size_t)s * nbar + i];
+      size_t at = ((size_t)(k0 * 3 + d) * W + s) * nbar + i;
+      Tv[at] = col < 0 ? 0.0 : Tv[at] * sr * sC[(size_t)kk * nbar + col];
+    }
+  }
+}
+
 void assemble_T(bbot_ctx* c) {
   DevGeom& g = c->g;
   Assembled& A = c->as;
   size_t nv = (size_t)g.K * 3 * g.W * g.nbar;
   if (A.Tv.n != nv) A.Tv.alloc(nv, c->dev.stream);
   A.precond = c->opts.precond;
-  if (c->opts.precond == 1) {
-    if (A.dAinv.n != (size_t)c->n()) A.dAinv.alloc(c->n(), c->dev.stream);
-    launch(c->dev, k_dainv, dim3(nblocks(c->n(), 256)), dim3(256), 0, c->n(), g.N, (const double*)A.Aoff.p,
-           A.dAinv.p);
+  if (c->opts.precond != 0) {
+    const bool hss = c->opts.precond == 2;
+    const long long n = c->n(), m = c->m();
+    if (A.dAinv.n != (size_t)n) A.dAinv.alloc(n, c->dev.stream);
+    launch(c->dev, k_dainv, dim3(nblocks(n, 256)), dim3(256), 0, n, g.N, (const double*)A.Aoff.p, A.dAinv.p);
+    const double* cd = A.Cd.p;
+    const double al = c->opts.alpha_hss;
+    if (hss) {     // scalings D^-1/2 and the diagonal alpha^2 C of alpha^2 C + B D_A^-1 B^T
+      if (A.sA.n != (size_t)n) A.sA.alloc(n, c->dev.stream);
+      if (A.sC.n != (size_t)m) { A.sC.alloc(m, c->dev.stream); A.c2.alloc(m, c->dev.stream); }
+      launch(c->dev, k_hss_scal, dim3(nblocks(std::max(n, m), 256)), dim3(256), 0, n, m, al,
+             (const double*)A.dAinv.p, (const double*)A.Cd.p, A.sA.p, A.sC.p, A.c2.p);
+      cd = A.c2.p;
+    }
     dim3 grid(nblocks(g.nbar, 128), (g.K + T_KCH - 1) / T_KCH);
     launch(c->dev, k_assemble_S, grid, dim3(128), 0, g.nbar, g.K, g.N, g.NE, g.W, g.dt, (const double*)g.c.p,
-           (const double*)A.gphi.p, (const double*)A.dAinv.p, (const double*)A.Cd.p, (const int*)g.fi_cell.p,
+           (const double*)A.gphi.p, (const double*)A.dAinv.p, cd, (const int*)g.fi_cell.p,
            (const int*)g.fi_child.p, (const int*)g.fi_edge.p, (const double*)g.fi_alpha.p, (const int*)g.fv_j.p,
            (const int*)g.fv_q.p, (const int*)g.fv_pos.p, A.Tv.p);
+    if (hss)       // S_K = alpha I + B^ B^T / alpha = (1/alpha) D_C^-1/2 (alpha^2 C + B D_A^-1 B^T) D_C^-1/2
+      launch(c->dev, k_hss_scale_S, dim3(nblocks((long long)g.K * g.nbar, 256)), dim3(256), 0, g.nbar, g.K, g.W,
+             1.0 / al, (const int*)g.tcol.p, (const double*)A.sC.p, A.Tv.p);
     return;
   }
   dim3 grid(nblocks(g.nbar, 128), (g.K + T_KCH - 1) / T_KCH);

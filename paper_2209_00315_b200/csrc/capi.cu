@@ -48,7 +48,8 @@ void check_opts(const bbot_solver_opts& o) {
   BB_REQUIRE(o.omega_A > 0 && o.omega_A < 2 && o.omega_T > 0 && o.omega_T < 2, BBOT_E_INPUT, "bad Jacobi weight");
   BB_REQUIRE(o.coarse_max_A >= 2 && o.coarse_max_A <= 120 && o.coarse_max_T >= 1 && o.coarse_max_T <= 8192,
              BBOT_E_INPUT, "bad coarse sizes");
-  BB_REQUIRE(o.precond == 0 || o.precond == 1, BBOT_E_INPUT, "precond must be 0 (BB) or 1 (SIMPLE)");
+  BB_REQUIRE(o.precond >= 0 && o.precond <= 2, BBOT_E_INPUT, "precond must be 0 (BB), 1 (SIMPLE) or 2 (HSS)");
+  BB_REQUIRE(o.alpha_hss > 0 && o.eps_in_hss > 0, BBOT_E_INPUT, "bad HSS alpha / eps_in");
   BB_REQUIRE(o.coarse_max_S >= 1 && o.coarse_max_S <= 8192, BBOT_E_INPUT, "bad coarse_max_S");
 }
 
@@ -71,6 +72,8 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->coarse_max_T = 1024;
   o->precond = 0;
   o->coarse_max_S = 256;
+  o->alpha_hss = 0.5;
+  o->eps_in_hss = 1e-1;
 }
 
 void bbot_default_ipm_opts(bbot_ipm_opts* o) {
@@ -268,7 +271,7 @@ bbot_status bbot_jp_matvec(bbot_ctx* c, const double* x, double* y, bbot_mem mem
   long long nm = c->n() + c->m();
   if (c->tmp_nm.n != (size_t)nm) { c->tmp_nm.alloc(nm, c->dev.stream); c->tmp_nm2.alloc(nm, c->dev.stream); }
   copy_in(c, c->tmp_nm.p, x, nm, mem);
-  if (c->as.precond == 1) j_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);   // SIMPLE: (eq:saddle-point)
+  if (c->as.precond != 0) j_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);   // SIMPLE / HSS: (eq:saddle-point)
   else jp_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);
   copy_out(c, y, c->tmp_nm2.p, nm, mem);
   sync(c->dev);
@@ -497,7 +500,8 @@ bbot_status bbot_amg_vcycle(bbot_ctx* c, int which, const double* b, double* x, 
   double* tb = which == 0 ? c->tmp_n.p : c->tmp_m.p;
   double* tx = which == 0 ? c->tmp_n2.p : c->tmp_m2.p;
   copy_in(c, tb, b, len, mem);
-  if (which == 0) amg_vcycle(c->dev, c->amgA, view_A(c), tb, tx);
+  if (which == 0 && c->as.precond == 2) amg_vcycle(c->dev, c->amgA, view_As(c), tb, tx);
+  else if (which == 0) amg_vcycle(c->dev, c->amgA, view_A(c), tb, tx);
   else amg_vcycle(c->dev, c->amgT, view_T(c), tb, tx);
   copy_out(c, x, tx, len, mem);
   sync(c->dev);

@@ -65,7 +65,8 @@ struct Assembled {
   DBuf<double> f, g, h, gt;       // RHS pieces
   DBuf<double> rhs;               // (f; P gt) (BB) or (f; gt) (SIMPLE)  (n+m)
   DBuf<double> Tv;                // [K][3][W][nbar]: T (BB) or S-hat = C + B diag(A)^-1 B^T (SIMPLE)
-  DBuf<double> dAinv;             // 1 / diag(A)  (n; SIMPLE)
+  DBuf<double> dAinv;             // 1 / diag(A)  (n; SIMPLE, HSS)
+  DBuf<double> sA, sC, c2;        // HSS: diag(A)^-1/2 (n), C^-1/2 (m), alpha^2 C (m)
   int precond = 0;                // preconditioner the assembly was built for
   double scale = 0;               // ||(f;g;h)||
   DBuf<double> dscale;            // the same on the device (read by the captured solve)

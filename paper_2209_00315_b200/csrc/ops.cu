@@ -221,6 +221,55 @@ void simple_out(bbot_ctx* c, const double* r, const double* z2, double* out) {
          (const double*)c->as.dAinv.p, z2, out);
 }
 
+// ---------------------------------------------------------------- NEXT f2: HSS
+// (oracle/hss.py; eq:prec-hss, eq:solve-K, eq:solve-laplacians)
+// -c = -(b + B^ a/alpha) with a = sA r1, b = -sC r2:  -c = sC (r2 - B(dAinv r1)/alpha)
+__global__ void k_hss_c(long long m, int nbar, double inv_alpha, BRow br, const double* __restrict__ r2,
+                        const double* __restrict__ w, const double* __restrict__ sC, double* __restrict__ negc) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  negc[t] = sC[t] * (r2[t] - br(w, k0, t - (long long)k0 * nbar) * inv_alpha);
+}
+__global__ void k_mul(long long n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) c[t] = a[t] * b[t];
+}
+// u = (a - B^T v)/alpha = sA (r1 - B^T(sC v))/alpha  (w = sC v)
+__global__ void k_hss_u(long long n, int N, double inv_alpha, BtRow bt, const double* __restrict__ r1,
+                        const double* __restrict__ w, const double* __restrict__ sA, double* __restrict__ u) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int kk = (int)(t / N);
+  u[t] = sA[t] * (r1[t] - bt(w, nullptr, 0.0, kk, t - (long long)kk * N)) * inv_alpha;
+}
+// z1 = sA x (in place), z2 = sC v / (1 + alpha)
+__global__ void k_hss_out(long long n, long long m, double inv_1pa, const double* __restrict__ sA,
+                          const double* __restrict__ sC, const double* __restrict__ v, double* __restrict__ z) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) z[t] *= sA[t];
+  else if (t < n + m) z[t] = sC[t - n] * v[t - n] * inv_1pa;
+}
+
+void hss_c(bbot_ctx* c, const double* r, double* negc) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_mul, dim3(nblocks(n, BS)), dim3(BS), 0, n, r, (const double*)c->as.dAinv.p, c->tmp_n.p);
+  launch(c->dev, k_hss_c, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, 1.0 / c->opts.alpha_hss, make_brow(c),
+         r + n, (const double*)c->tmp_n.p, (const double*)c->as.sC.p, negc);
+}
+void hss_u(bbot_ctx* c, const double* r, const double* v, double* w, double* u) {
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_mul, dim3(nblocks(m, BS)), dim3(BS), 0, m, v, (const double*)c->as.sC.p, w);
+  launch(c->dev, k_hss_u, dim3(nblocks(n, BS)), dim3(BS), 0, n, c->g.N, 1.0 / c->opts.alpha_hss, make_btrow(c), r,
+         (const double*)w, (const double*)c->as.sA.p, u);
+}
+void hss_out(bbot_ctx* c, const double* v, double* z) {
+  long long n = c->n(), m = c->m();
+  launch(c->dev, k_hss_out, dim3(nblocks(n + m, BS)), dim3(BS), 0, n, m, 1.0 / (1.0 + c->opts.alpha_hss),
+         (const double*)c->as.sA.p, (const double*)c->as.sC.p, v, z);
+}
+
 // ---------------------------------------------------------------- y = T x, y = A x
 template <class V>
 __global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y) {
@@ -365,7 +414,7 @@ void set_user_rhs(bbot_ctx* c) {   // as.f, as.g, as.h hold the caller's (f; g; 
   launch(c->dev, k_user_gt, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, (const double*)g.cbar.p,
          (const double*)A.g.p, (const double*)A.h.p, (const double*)(c->rho_ext.p + g.nbar), A.gt.p);
   BB_CUDA(cudaMemcpyAsync(A.rhs.p, A.f.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (A.precond == 1) {
+  if (A.precond != 0) {
     BB_CUDA(cudaMemcpyAsync(A.rhs.p + n, A.gt.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
   } else {
     c->red.slice_sum(WSlice{nullptr, A.gt.p, g.nbar}, g.nbar, K, sc + 3 * K + 1, false);
@@ -424,7 +473,7 @@ void recover(bbot_ctx* c) {
   long long n = c->n(), m = c->m();
   int K = g.K;
   cudaStream_t s = c->dev.stream;
-  if (c->as.precond == 1) {    // SIMPLE on (eq:saddle-point): dphi = x1, drho = x2, ds
+  if (c->as.precond != 0) {    // SIMPLE / HSS on (eq:saddle-point): dphi = x1, drho = x2, ds
     BB_CUDA(cudaMemcpyAsync(c->dphi.p, c->sol.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     BB_CUDA(cudaMemcpyAsync(c->drho.p, c->sol.p + n, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
     launch(c->dev, k_ds, dim3(nblocks(m, BS)), dim3(BS), 0, m, (const double*)c->as.h.p, (const double*)c->s.p,

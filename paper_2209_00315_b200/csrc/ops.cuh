@@ -11,6 +11,7 @@ void assemble_edges(bbot_ctx* c);                    // omega, gphi, omegabar, C
 void compute_residual(bbot_ctx* c, bool write_rhs);  // F (as f,g,h = -F), g~, rhs, norms
 void assemble_T(bbot_ctx* c);                        // T values
 LapView view_A(bbot_ctx* c);
+ScaledLapView view_As(bbot_ctx* c);                  // HSS: A^ + alpha I
 SliceEllView view_T(bbot_ctx* c);
 
 // ops.cu
@@ -22,6 +23,9 @@ void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L);         // 
 void j_matvec(bbot_ctx* c, const double* x, double* y);                     // (eq:saddle-point)
 void simple_c(bbot_ctx* c, const double* r, double* z1, double* cvec);      // z1 = diag(A)^-1 r1, c = r2 - B z1
 void simple_out(bbot_ctx* c, const double* r, const double* z2, double* out);  // (diag(A)^-1(r1 - B^T z2); z2)
+void hss_c(bbot_ctx* c, const double* r, double* negc);                     // -c = sC (r2 - B(dAinv r1)/alpha)
+void hss_u(bbot_ctx* c, const double* r, const double* v, double* w, double* u);   // u = sA (r1 - B^T(sC v))/alpha
+void hss_out(bbot_ctx* c, const double* v, double* z);                      // z1 *= sA, z2 = sC v/(1+alpha)
 void set_user_rhs(bbot_ctx* c);                                            // solve(rhs): (f;g;h) in as.f/g/h
 void finish_user_solve(bbot_ctx* c);                                       // drho += drho0
 void recover(bbot_ctx* c);                                                   // a6

@@ -57,6 +57,9 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
   if (c->as.precond == 1) {   // SIMPLE: one hierarchy, on S-hat (the A block is inverted by its diagonal)
     c->amgA.clear();
     amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_S, w);
+  } else if (c->as.precond == 2) {   // HSS: AMG(A^ + alpha I) per slice (mode As) + AMG(S_K) across time
+    amg_setup(c->dev, c->amgA, view_As(c), c->g.slice_A.p, c->g.K + 1, 2, o.omega_A, o.coarse_max_A, w);
+    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_S, w);
   } else if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
     amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
     amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
@@ -174,8 +177,34 @@ static void emit_simple_apply(bbot_ctx* c, const double* r, double* z) {
   simple_out(c, r, c->tmp_m2.p, z);
 }
 
+// NEXT f2: z = HSS(r) (eq:prec-hss with the diagonal scaling; oracle/hss.py):
+//   -c = sC (r2 - B(dAinv r1)/alpha);  S_K v = c by GMRES(restart_T) + AMG(S_K), eps_in_hss;
+//   u = sA (r1 - B^T(sC v))/alpha;  (A^ + alpha I) x = u per slice by PCG + AMG, eps_in_hss;
+//   z = (sA x; sC v/(1+alpha))
+static void emit_hss_apply(bbot_ctx* c, const double* r, double* z) {
+  const bbot_solver_opts& o = c->opts;
+  long long m = c->m();
+  hss_c(c, r, c->tmp_m2.p);
+  dev_neg_norm(c->dev, c->red, c->tmp_m2.p, c->tmp_m.p, m, c->nrm_T.p);
+  SliceEllView vS = view_T(c);
+  c->innerT.emit(
+      c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
+      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgT, vS, x, y); }, c->tmp_m.p, c->tmp_m2.p,
+      c->nrm_T.p, o.eps_in_hss, o.maxit_inner);
+  hss_u(c, r, c->tmp_m2.p, c->tmp_m.p, c->tmp_n2.p);
+  ScaledLapView vH = view_As(c);
+  c->pcg.emit(
+      c->dev, c->red, vH,
+      [&](const double* x, double* y, const SliceDotFuse* f) {
+        return amg_vcycle(c->dev, c->amgA, vH, x, y, f, f ? f->active : nullptr);
+      },
+      c->tmp_n2.p, z, c->g.N, o.eps_in_hss, o.maxit_inner);
+  hss_out(c, c->tmp_m2.p, z);
+}
+
 static void emit_apply(bbot_ctx* c, const double* r, double* z) {
   if (c->as.precond == 1) emit_simple_apply(c, r, z);
+  else if (c->as.precond == 2) emit_hss_apply(c, r, z);
   else emit_bb_apply(c, r, z);
 }
 
@@ -184,7 +213,7 @@ static void emit_solve(bbot_ctx* c) {
   const bbot_solver_opts& o = c->opts;
   c->innerT.reset_total(c->dev);
   c->pcg.reset_stats(c->dev);
-  const bool simple = c->as.precond == 1;
+  const bool simple = c->as.precond != 0;   // SIMPLE and HSS: the saddle-point system
   c->outer.emit(
       c->dev, c->red,
       [&](const double* x, double* y) {

@@ -61,8 +61,12 @@ def main(rep, config, out_txt):
     open(out_txt, "w").write("\n".join(lines) + "\n")
     js = os.path.join(ROOT, "profiles", "ncu_summary.json")
     data = json.load(open(js)) if os.path.exists(js) else {}
-    data.setdefault("dram_bytes_per_launch", {})[config] = summary
-    data.setdefault("sources", {})[config] = os.path.basename(out_txt)
+    data.setdefault("dram_bytes_per_launch", {}).setdefault(config, {}).update(summary)   # merge per kernel
+    src = data.setdefault("sources", {}).get(config, [])
+    src = src if isinstance(src, list) else [src]
+    data["sources"][config] = src + [os.path.basename(out_txt)]
+    rnd = os.path.basename(out_txt).split("_")[0]
+    data.setdefault("round", {}).update({f"{config}/{k}": rnd for k in summary})
     json.dump(data, open(js, "w"), indent=1)
     print("\n".join(lines))
 
