@@ -238,23 +238,35 @@ bbot_status bbot_amg_vcycle(bbot_ctx* ctx, int which, const double* b, double* x
  * (kernels replayed from the solve's CUDA graph are not counted; run the same
  * solve with bbot_set_exec_mode(ctx, 0) or under the profiler to count them). */
 long long bbot_launch_count(const bbot_ctx* ctx);
-/* Multi-GPU time slabs, one process per GPU.
- * Rank r owns a contiguous slab [k_begin, k_end) of the K+1 potential slices
- * (sizes differ by at most one).  The per-slice A_k solves of every BB apply
- * ((4.20), P:1469 -- independent per time slice) run on the owned slices
- * only and are then exchanged with NCCL (one grouped broadcast per slab, on the
- * context stream, inside the apply); every other step is computed redundantly and
- * deterministically on all ranks, so every rank holds the same iterate, bitwise
- * equal to the single-GPU run.  Multi-rank solves are issued eagerly (NCCL is not
- * captured into the conditional-node solve graph).  Inner-A statistics become
- * per-rank.  Memory is NOT divided by the rank count in this scope.
+/* Multi-GPU time slabs ("well suited for
+ * parallelization"), one rank per GPU.  Rank r owns the potential slices [k_begin, k_end)
+ * = [floor(r(K+1)/P), floor((r+1)(K+1)/P)) and the density slices [k_begin, min(k_end, K));
+ * 2P <= K+1.  The Newton SOLVE is decomposed: the FGMRES and T-GMRES Krylov vectors, J_P
+ * (4.17), the T-solve (T SpMV and every grid-wide level of the AMG(T) V-cycle), the BB glue
+ * (4.18)-(4.20), the per-slice A_k PCG solves and the recovery (a6) run on the owned slices,
+ * with one-slice halo exchanges (x1 from the right and x2, y from the left for J_P, B, B^T;
+ * z from both sides for T and for each AMG(T) level; dphit from the right for the delta-lambda
+ * sums) and allgathers of per-slice reduction totals: every dot / norm is the in-order sum of
+ * per-slice totals whose block partition depends only on the slice length, so the result is
+ * bitwise equal to the single-GPU solve for every P.  The coarse AMG(T) tail (<= 16384 rows)
+ * runs redundantly on the allgathered level.  Replicated (every rank, bitwise equal): the
+ * state, assembly, AMG setups, the Newton update (the direction is allgathered after the
+ * recovery).  Memory is not divided in this scope (global-layout vectors on every rank).
+ * Multi-rank solves are issued eagerly (host-driven loops; BB preconditioner only).
  * bbot_nccl_unique_id: on rank 0; the caller broadcasts the 128 bytes.
- * bbot_set_dist: after bbot_create, before bbot_assemble; uid == NULL makes a
- * "virtual rank" (the partition without communication: non-owned slices of the
- * A_k solutions stay 0) for testing the partition on one GPU. */
+ * bbot_set_dist: after bbot_create, before bbot_assemble (NCCL, uid required for P > 1).
+ * bbot_set_dist_virtual: P contexts of ONE process (one host thread per rank, each calling
+ * the same sequence of API calls concurrently) exchanging by device-to-device copies through
+ * a process-wide group `group` -- the decomposition on a single GPU, for testing. */
 bbot_status bbot_nccl_unique_id(unsigned char out[128]);
 bbot_status bbot_set_dist(bbot_ctx* ctx, int rank, int nranks, const unsigned char* uid);
+bbot_status bbot_set_dist_virtual(bbot_ctx* ctx, int rank, int nranks, long long group);
 bbot_status bbot_get_slab(const bbot_ctx* ctx, int* k_begin, int* k_end);
+/* The ownership rule of the exchange layer (host only, no GPU): rank `rank` of `nranks` owns
+ * the slices [*lo, *hi) of a slice-structured vector with S slices when the slabs are cut
+ * over Kp1 = K+1 potential slices; its halos are slices *lo-1 (from rank-1) and *hi (from
+ * rank+1).  For the exchange-plan tests. */
+bbot_status bbot_slab_plan(int Kp1, int nranks, int rank, int S, int* lo, int* hi);
 
 /* Execution mode of bbot_solve.  1 (default): the whole solve -- FGMRES, the BB
  * applies with their inner GMRES / per-slice PCG loops, recovery -- is captured

@@ -7,7 +7,9 @@ ctypes binding.  Importing it without the built library raises ImportError --
 there is deliberately no CPU fallback.
 """
 from ._bbot import (BBOT_MEM_DEVICE, BBOT_MEM_HOST, EXPORTED, LIB_PATH, BbotError, Context, IpmOpts,
-                    SolveStats, SolverOpts, default_ipm_opts, default_solver_opts, lib, nccl_unique_id)
+                    SolveStats, SolverOpts, default_ipm_opts, default_solver_opts, lib, nccl_unique_id,
+                    slab_plan)
 
 __all__ = ["Context", "SolverOpts", "IpmOpts", "SolveStats", "BbotError", "default_solver_opts",
-           "default_ipm_opts", "lib", "LIB_PATH", "EXPORTED", "BBOT_MEM_HOST", "BBOT_MEM_DEVICE", "nccl_unique_id"]
+           "default_ipm_opts", "lib", "LIB_PATH", "EXPORTED", "BBOT_MEM_HOST", "BBOT_MEM_DEVICE", "nccl_unique_id",
+           "slab_plan"]

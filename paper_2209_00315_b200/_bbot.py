@@ -102,7 +102,9 @@ _sigs = {
     "bbot_set_exec_mode": (C.c_int, [_P, C.c_int]),
     "bbot_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "bbot_set_dist": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
+    "bbot_set_dist_virtual": (C.c_int, [_P, C.c_int, C.c_int, C.c_longlong]),
     "bbot_get_slab": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "bbot_slab_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bbot_prof_start": (C.c_int, [_P]),
     "bbot_prof_stop": (C.c_int, [_P, C.c_char_p, C.c_longlong, C.POINTER(C.c_longlong)]),
 }
@@ -126,6 +128,15 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise BbotError(st, "bbot_nccl_unique_id failed (see stderr)")
     return buf.raw
+
+
+def slab_plan(Kp1: int, nranks: int, rank: int, S: int):
+    """(lo, hi): the slices of an S-slice vector that `rank` owns (bbot_slab_plan)."""
+    lo, hi = C.c_int(), C.c_int()
+    st = lib.bbot_slab_plan(int(Kp1), int(nranks), int(rank), int(S), C.byref(lo), C.byref(hi))
+    if st != 0:
+        raise BbotError(st, "bbot_slab_plan: bad arguments")
+    return lo.value, hi.value
 
 
 def default_solver_opts(**kw) -> SolverOpts:
@@ -353,11 +364,15 @@ class Context:
         return lib.bbot_launch_count(self._h)
 
     def set_dist(self, rank: int, nranks: int, uid: bytes | None):
-        """Time-slab partition of the A_k solves (uid: 128 bytes from nccl_unique_id() on
-        rank 0, or None for a virtual rank without communication)."""
+        """Time-slab decomposition over NCCL (uid: 128 bytes from nccl_unique_id() on rank 0)."""
         if uid is not None and len(uid) != 128:
             raise ValueError("uid must be 128 bytes")
         self._check(lib.bbot_set_dist(self._h, int(rank), int(nranks), uid))
+
+    def set_dist_virtual(self, rank: int, nranks: int, group: int):
+        """Time-slab decomposition among the contexts of THIS process sharing `group` (device-to-
+        device exchange; each rank's calls must run concurrently, one thread per rank)."""
+        self._check(lib.bbot_set_dist_virtual(self._h, int(rank), int(nranks), int(group)))
 
     def slab(self):
         a, b = C.c_int(), C.c_int()

@@ -3,6 +3,7 @@
 // DESIGN.md §2 (I3); the oracle (oracle/amg.py) implements the same algorithm
 // independently.
 #include "amg.cuh"
+#include "comm.cuh"
 #include <climits>
 #include <cooperative_groups.h>
 #include <chrono>
@@ -302,9 +303,9 @@ __global__ void k_slice_ptr(long long n, const int* __restrict__ sl, int nslices
 // ------------------------------------------------------------ V-cycle kernels
 template <class V>
 __global__ void k_down(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
-                       double* __restrict__ x, double* __restrict__ res, SliceSkip sk) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows || sk.skip(r)) return;
+                       double* __restrict__ x, double* __restrict__ res, SliceSkip sk, RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rr.r1 || sk.skip(r)) return;
   double acc = b[r];
   v.row(r, [&](long long c, double a) { acc -= a * (om * dinv[c] * b[c]); });
   x[r] = om * dinv[r] * b[r];
@@ -312,9 +313,9 @@ __global__ void k_down(V v, const double* __restrict__ dinv, const double* __res
 }
 
 __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
-                           const double* __restrict__ r, double* bc, SliceSkip sk) {
-  long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= nc || sk.skip(I)) return;
+                           const double* __restrict__ r, double* bc, SliceSkip sk, RowRange rr) {
+  long long I = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= rr.r1 || sk.skip(I)) return;
   double acc = 0.0;
   for (long long p = mptr[I]; p < mptr[I + 1]; p++) acc += r[midx[p]];   // P^T r, members ascending
   bc[I] = acc;
@@ -325,14 +326,15 @@ __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, con
 // pre-smoothing x = om D^-1 b first, then the residual sweep reads x (same
 // expression order as k_down: bitwise identical), one gather per entry
 __global__ void k_jacobi0(long long n, const double* __restrict__ dinv, const double* __restrict__ b, double om,
-                          double* __restrict__ x) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) x[r] = om * dinv[r] * b[r];
+                          double* __restrict__ x, RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rr.r1) x[r] = om * dinv[r] * b[r];
 }
 template <class V>
-__global__ void k_resid(V v, const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ res) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows) return;
+__global__ void k_resid(V v, const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ res,
+                        RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rr.r1) return;
   double acc = b[r];
   v.row(r, [&](long long c, double a) { acc -= a * x[c]; });
   res[r] = acc;
@@ -342,9 +344,9 @@ __global__ void k_resid(V v, const double* __restrict__ b, const double* __restr
 // two launches instead of k_up's chained gathers (neighbour -> agg -> xc) on each of
 // T's ~27 entries per row; the same sums in the same order (bitwise identical)
 __global__ void k_prolong(long long n, const double* __restrict__ x, const int* __restrict__ agg,
-                          const double* __restrict__ xc, double* __restrict__ xp, SliceSkip sk) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n && !sk.skip(r)) xp[r] = x[r] + xc[agg[r]];
+                          const double* __restrict__ xc, double* __restrict__ xp, SliceSkip sk, RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rr.r1 && !sk.skip(r)) xp[r] = x[r] + xc[agg[r]];
 }
 
 // AMG(A) level 0 after k_prolong: post-smoothing on xp fused with the per-slice dot
@@ -370,9 +372,9 @@ __global__ void k_post_dot(V v, const double* __restrict__ dinv, const double* _
 }
 template <class V>
 __global__ void k_post(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
-                       const double* __restrict__ xp, double* __restrict__ xo) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows) return;
+                       const double* __restrict__ xp, double* __restrict__ xo, RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rr.r1) return;
   double acc = b[r];
   v.row(r, [&](long long c, double a) { acc -= a * xp[c]; });
   xo[r] = xp[r] + om * dinv[r] * acc;
@@ -732,13 +734,15 @@ struct TailTArgs {
   TailTLevel lv[TAIL_MAXL];
 };
 
-__global__ void __launch_bounds__(TAIL_BS) k_tailT(const TailTArgs* __restrict__ T) {
+// restrict_first = 0: level `first`'s right-hand side is already in place (time slabs:
+// restricted slab by slab, then allgathered)
+__global__ void __launch_bounds__(TAIL_BS) k_tailT(const TailTArgs* __restrict__ T, int restrict_first) {
   cg::cluster_group cl = cg::this_cluster();
   const long long g0 = (long long)cl.block_rank() * blockDim.x + threadIdx.x;
   const long long gs = (long long)cl.num_blocks() * blockDim.x;
   const double om = T->om;
   const int nl = T->last - T->first;
-  {
+  if (restrict_first) {
     const TailTLevel& F = T->lv[0];
     for (long long I = g0; I < F.n; I += gs) {
       double acc = 0.0;
@@ -1317,7 +1321,8 @@ static void coarse_solve(Dev& d, AmgHierarchy& H, const double* b, double* x) {
     launch(d, k_coarseA_apply, dim3(H.nslices), dim3(128), 0, (const long long*)H.csptr.p, H.cm,
            (const double*)H.cinv.p, b, x, H.mode == 0 ? 1 : 0);
   else if (H.cjac)
-    launch(d, k_jacobi0, dim3(nblocks(C.n, 256)), dim3(256), 0, C.n, (const double*)C.dinv.p, b, H.omega, x);
+    launch(d, k_jacobi0, dim3(nblocks(C.n, 256)), dim3(256), 0, C.n, (const double*)C.dinv.p, b, H.omega, x,
+           RowRange{0, C.n});
   else
     launch(d, k_dense_mv, dim3(nblocks((long long)C.n * 32, 256)), dim3(256), 0, (int)C.n,
            (const double*)H.cinv.p, b, x);
@@ -1377,23 +1382,24 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     AmgLevel& lv = H.lv[l];
     unsigned nb = nblocks(lv.n, BS);
     if (l == 0 && H.mode == 1) {   // T level 0: Jacobi step first, then a plain residual sweep
-      launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p);
-      launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p);
+      launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, RowRange{0, lv.n});
+      launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, RowRange{0, lv.n});
     } else if (l == 0)
-      launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0));
+      launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
+             RowRange{0, lv.n});
     else
       launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
-             (const double*)lv.b.p, om, lv.x.p, lv.r.p, skip_at(l));
+             (const double*)lv.b.p, om, lv.x.p, lv.r.p, skip_at(l), RowRange{0, lv.n});
     if (!(H.tail > 0 && l == stop - 1))
       launch(d, k_restrict, dim3(nblocks(lv.nc, BS)), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p,
-             (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1));
+             (const int*)lv.midx.p, (const double*)lv.r.p, H.lv[l + 1].b.p, skip_at(l + 1), RowRange{0, lv.nc});
   }
   if (H.mode != 1 && H.tail > 0) {
     int cl = TAIL_CL > 0 ? std::min(TAIL_CL, TAIL_MAXCL)
                          : std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
     launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(TAIL_BS), 0, cl, (const TailArgs*)H.tail_args.p, active);
   } else if (H.tail > 0) {
-    launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p);
+    launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p, 1);
   } else {
     coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
   }
@@ -1404,7 +1410,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     const double* xc = level_out(H, l + 1);
     if (l == 0 && fuse && UP_SPLIT) {     // prolongate first, then the sweep fused with r.z
       launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p,
-             skip_at(0));
+             skip_at(0), RowRange{0, lv.n});
       launch(d, k_post_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.xt.p, out, fuse->L, fuse->R, fuse->fin, active);
     } else if (l == 0 && fuse) {
@@ -1412,8 +1418,9 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
              (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);
     } else if (l == 0 && H.mode == 1) {   // T level 0: prolongate first, then a plain sweep
       launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.xt.p,
-             SliceSkip{nullptr, nullptr, 1});
-      launch(d, k_post<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.xt.p, out);
+             SliceSkip{nullptr, nullptr, 1}, RowRange{0, lv.n});
+      launch(d, k_post<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.xt.p, out,
+             RowRange{0, lv.n});
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
              (const int*)lv.agg.p, xc, out, skip_at(0));
@@ -1423,6 +1430,69 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     }
   }
   return fuse != nullptr;
+}
+
+template <class V0>
+void amg_vcycle_slab(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, Comm& comm, int ra, int rb) {
+  BB_REQUIRE(H.mode == 1, BBOT_E_INTERNAL, "amg_vcycle_slab: mode-T hierarchies only");
+  const int L = (int)H.lv.size();
+  const double om = H.omega;
+  auto lay = [&](int l) {
+    Layout Ly;
+    Ly.off = H.lv[l].sptr;
+    return Ly;
+  };
+  auto rng = [&](int l) { return RowRange{H.lv[l].sptr[ra], H.lv[l].sptr[rb]}; };
+  auto grid = [&](const RowRange& r) { return dim3(nblocks(std::max(1LL, r.r1 - r.r0), BS)); };
+  const SliceSkip none{nullptr, nullptr, 1};
+  if (L == 1) {                        // level 0 is the coarsest: solve it redundantly
+    AmgLevel& C = H.lv[0];
+    RowRange r = rng(0);
+    if (r.r1 > r.r0)
+      BB_CUDA(cudaMemcpyAsync(C.b.p + r.r0, b + r.r0, (r.r1 - r.r0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                              d.stream));
+    comm.allgather(d, lay(0), C.b.p);
+    coarse_solve(d, H, C.b.p, x);
+    return;
+  }
+  const int stop = H.tail > 0 ? H.tail : L - 1;
+  for (int l = 0; l < stop; l++) {
+    AmgLevel& lv = H.lv[l];
+    RowRange r = rng(l);
+    if (l == 0) {
+      launch(d, k_jacobi0, grid(r), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, r);
+      comm.halo(d, lay(0), lv.x.p);
+      launch(d, k_resid<V0>, grid(r), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, r);
+    } else {
+      comm.halo(d, lay(l), lv.b.p);
+      launch(d, k_down<SellView>, grid(r), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p, (const double*)lv.b.p,
+             om, lv.x.p, lv.r.p, none, r);
+    }
+    RowRange rc = rng(l + 1);
+    launch(d, k_restrict, grid(rc), dim3(BS), 0, lv.nc, (const long long*)lv.mptr.p, (const int*)lv.midx.p,
+           (const double*)lv.r.p, H.lv[l + 1].b.p, none, rc);
+  }
+  if (H.tail > 0) {
+    comm.allgather(d, lay(H.tail), H.lv[H.tail].b.p);
+    launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p, 0);
+  } else {
+    comm.allgather(d, lay(L - 1), H.lv[L - 1].b.p);
+    coarse_solve(d, H, H.lv[L - 1].b.p, H.lv[L - 1].x.p);
+  }
+  for (int l = stop - 1; l >= 0; l--) {
+    AmgLevel& lv = H.lv[l];
+    RowRange r = rng(l);
+    double* out = l == 0 ? x : level_out(H, l);
+    const double* xc = level_out(H, l + 1);
+    double* tmp = l == 0 ? lv.xt.p : lv.r.p;      // the prolongated iterate x + P xc
+    launch(d, k_prolong, grid(r), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, tmp, none, r);
+    comm.halo(d, lay(l), tmp);
+    if (l == 0)
+      launch(d, k_post<V0>, grid(r), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)tmp, out, r);
+    else
+      launch(d, k_post<SellView>, grid(r), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p, (const double*)lv.b.p,
+             om, (const double*)tmp, out, r);
+  }
 }
 
 template void amg_setup<LapView>(Dev&, AmgHierarchy&, const LapView&, const int*, int, int, double, int,
@@ -1437,5 +1507,7 @@ template bool amg_vcycle<ScaledLapView>(Dev&, AmgHierarchy&, const ScaledLapView
                                         const SliceDotFuse*, const double*);
 template bool amg_vcycle<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*,
                                        const SliceDotFuse*, const double*);
+template void amg_vcycle_slab<SliceEllView>(Dev&, AmgHierarchy&, const SliceEllView&, const double*, double*, Comm&,
+                                            int, int);
 
 }  // namespace bbot

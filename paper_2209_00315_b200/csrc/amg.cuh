@@ -181,6 +181,11 @@ struct SliceSkip {
   }
 };
 
+// rows [r0, r1) of a level a launch covers (time slabs: the rank's own slices)
+struct RowRange {
+  long long r0, r1;
+};
+
 struct AmgLevel {
   long long n = 0, nc = 0;
   // CSR (levels >= 1)
@@ -240,5 +245,13 @@ void amg_setup(Dev& d, AmgHierarchy& H, const V0& v0, const int* slice0, int nsl
 template <class V0>
 bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x,
                 const SliceDotFuse* fuse = nullptr, const double* active = nullptr);
+// The V-cycle of a mode-T hierarchy (AMG(T)) on the time slab of a multi-rank context: every
+// grid-wide level sweeps its own slices' rows [ra, rb) (slice-grouped coarse rows) after a
+// one-slice halo exchange of the vector the sweep gathers from; the coarse tail (or the
+// coarsest solve) runs redundantly on every rank on the allgathered input.  Same sums in the
+// same order as amg_vcycle (bitwise equal to the single-GPU cycle).
+class Comm;
+template <class V0>
+void amg_vcycle_slab(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, Comm& comm, int ra, int rb);
 
 }  // namespace bbot

@@ -41,6 +41,13 @@ void copy_out(bbot_ctx* c, double* dst, const double* src, long long n, bbot_mem
                           mem == BBOT_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->dev.stream));
   if (mem == BBOT_MEM_HOST) sync(c->dev);
 }
+// time slabs: the owned slices of an (n+m) vector to every rank (whole-vector API outputs)
+void allgather_nm(bbot_ctx* c, double* v) {
+  if (!c->slab()) return;
+  c->comm->allgather(c->dev, Layout::uniform(c->g.K + 1, c->g.N), v);
+  c->comm->allgather(c->dev, Layout::uniform(c->g.K, c->g.nbar), v + c->n());
+}
+
 void check_opts(const bbot_solver_opts& o) {
   BB_REQUIRE(o.eps_out > 0 && o.eps_T > 0 && o.eps_A > 0, BBOT_E_INPUT, "tolerances must be > 0");
   BB_REQUIRE(o.restart >= 1 && o.restart <= GM_MAXR && o.maxit >= 1, BBOT_E_INPUT, "bad FGMRES restart/maxit");
@@ -273,6 +280,7 @@ bbot_status bbot_jp_matvec(bbot_ctx* c, const double* x, double* y, bbot_mem mem
   copy_in(c, c->tmp_nm.p, x, nm, mem);
   if (c->as.precond != 0) j_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);   // SIMPLE / HSS: (eq:saddle-point)
   else jp_matvec(c, c->tmp_nm.p, c->tmp_nm2.p);
+  allgather_nm(c, c->tmp_nm2.p);    // time slabs: every rank returns the whole product
   copy_out(c, y, c->tmp_nm2.p, nm, mem);
   sync(c->dev);
   API_END(c)
@@ -287,6 +295,7 @@ bbot_status bbot_bb_apply(bbot_ctx* c, const double* r, double* z, bbot_mem mem,
   if (c->tmp_nm.n != (size_t)nm) { c->tmp_nm.alloc(nm, c->dev.stream); c->tmp_nm2.alloc(nm, c->dev.stream); }
   copy_in(c, c->tmp_nm.p, r, nm, mem);
   bb_apply(c, c->tmp_nm.p, c->tmp_nm2.p, inner_T_its, inner_A_its_max);
+  allgather_nm(c, c->tmp_nm2.p);
   copy_out(c, z, c->tmp_nm2.p, nm, mem);
   sync(c->dev);
   API_END(c)
@@ -524,8 +533,22 @@ bbot_status bbot_nccl_unique_id(unsigned char out[128]) {
 bbot_status bbot_set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid) {
   if (!c) return BBOT_E_INPUT;
   API_BEGIN(c)
-  set_dist(c, rank, nranks, uid);
+  BB_REQUIRE(uid != nullptr || nranks == 1, BBOT_E_INPUT, "bbot_set_dist: NCCL unique id required (nranks > 1)");
+  set_dist(c, rank, nranks, uid, 0);
   API_END(c)
+}
+
+bbot_status bbot_set_dist_virtual(bbot_ctx* c, int rank, int nranks, long long group) {
+  if (!c) return BBOT_E_INPUT;
+  API_BEGIN(c)
+  set_dist(c, rank, nranks, nullptr, group);
+  API_END(c)
+}
+
+bbot_status bbot_slab_plan(int Kp1, int nranks, int rank, int S, int* lo, int* hi) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || S < 0 || !lo || !hi) return BBOT_E_INPUT;
+  slab_owned(Kp1, nranks, rank, S, *lo, *hi);
+  return BBOT_OK;
 }
 
 bbot_status bbot_get_slab(const bbot_ctx* c, int* k_begin, int* k_end) {

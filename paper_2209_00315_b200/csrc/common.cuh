@@ -260,8 +260,9 @@ __device__ __forceinline__ double block_min(double v) {
 struct RedArgs {
   double* partial;
   unsigned* counter;
-  double* out;
+  double* out;       // per-slice results of the launched slices (out[0] = slice k0)
   int parts;
+  int k0;            // first slice of the launch (time slabs: a rank launches its own slices)
 };
 
 // Called by all threads of every block after the block's partial(s) are written
@@ -325,7 +326,7 @@ struct SqrtFin {   // out[k] = sqrt(out[k])
 // out[k] = sum_{i < len} f(k, i); then fin(out) in the last block (all threads).
 template <class F, class Fin>
 __global__ void k_slice_reduce(F f, long long len, RedArgs R, Fin fin) {
-  int k = blockIdx.y;
+  int k = R.k0 + blockIdx.y;
   long long beg, end;
   red_chunk(len, R.parts, beg, end);
   double acc = 0.0;
@@ -371,9 +372,9 @@ struct Reducer {
     p = std::min(p, 4096LL);
     return (int)std::max(1LL, p);
   }
-  RedArgs args(int parts, int nslices, double* out) {
+  RedArgs args(int parts, int nslices, double* out, int k0 = 0) {
     if ((size_t)parts * nslices > cap) throw Error(BBOT_E_INTERNAL, "reduction workspace too small");
-    return RedArgs{partial.p, counter.p, out, parts};
+    return RedArgs{partial.p, counter.p, out, parts, k0};
   }
   template <class F, class Fin>
   void reduce(F f, long long len, int nslices, double* out, Fin fin) {
@@ -384,6 +385,16 @@ struct Reducer {
   void slice_sum(F f, long long len, int nslices, double* out, bool take_sqrt = false) {
     if (take_sqrt) reduce(f, len, nslices, out, SqrtFin{out, nslices});
     else reduce(f, len, nslices, out, NoFin{});
+  }
+  // per-slice sums of the slices [k_lo, k_hi) of an ns_total-slice vector into out[k] (global
+  // index); the partition into blocks depends on (len, ns_total) only, so a slab's results are
+  // bitwise those of the full launch (time slabs)
+  template <class F>
+  void slice_sum_range(F f, long long len, int k_lo, int k_hi, int ns_total, double* out) {
+    if (k_hi <= k_lo) return;
+    int parts = parts_for(len, ns_total);
+    launch(*dev, k_slice_reduce<F, NoFin>, dim3(parts, k_hi - k_lo), dim3(BS), 0, f, len,
+           args(parts, k_hi - k_lo, out + k_lo, k_lo), NoFin{});
   }
   template <class F>
   void slice_min(F f, long long len, int nslices, double* out) {

@@ -11,6 +11,7 @@
 #include "geometry.h"
 #include "amg.cuh"
 #include "krylov.cuh"
+#include "comm.cuh"
 #include <string>
 #include <memory>
 
@@ -113,10 +114,15 @@ struct bbot_ctx {
   bbot::DBuf<double> scal;      // device scalars / per-slice scratch (>= 8*(K+2))
   bbot::DBuf<long long> scan_ws;
   bbot::DBuf<double> nrm_T;      // ||r2|| of the current BB apply (device scalar)
-  // multi-GPU time slabs (dist.cu): owned potential slices [own_begin, own_end)
+  // multi-GPU time slabs (dist.cu, comm.cuh): owned potential slices [own_begin, own_end)
   int rank = 0, nranks = 1, own_begin = 0, own_end = 1 << 30;
-  bool virt = false;             // virtual rank (no communication; partition tests on one GPU)
-  void* comm = nullptr;          // ncclComm_t
+  std::unique_ptr<bbot::Comm> comm;   // NCCL or virtual exchange layer (nranks > 1)
+  bool slab() const { return nranks > 1; }
+  // owned slices: potential [pa, pb), density [ra, rb)  (all of them on one rank)
+  int pa() const { return slab() ? own_begin : 0; }
+  int pb() const { return slab() ? own_end : g.K + 1; }
+  int ra() const { return std::min(pa(), g.K); }
+  int rb() const { return std::min(pb(), g.K); }
   long long n() const { return (long long)g.N * (g.K + 1); }
   long long m() const { return (long long)g.nbar * g.K; }
 };

@@ -23,19 +23,6 @@ __global__ void k_axpby(double alpha, const double* __restrict__ a, double beta,
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = alpha * a[i] + beta * b[i];
 }
-__global__ void k_neg_norm(long long n, const double* __restrict__ a, double* __restrict__ b, RedArgs R,
-                           double* norm) {
-  long long beg, end;
-  red_chunk(n, R.parts, beg, end);
-  double acc = 0.0;
-  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    double v = a[i];
-    b[i] = -v;
-    acc += v * v;
-  }
-  if (red_commit(acc, R) && threadIdx.x == 0) *norm = sqrt(R.out[0]);
-}
-
 void dev_copy(Dev& d, const double* a, double* b, long long n) {
   launch(d, k_copy, dim3(nblocks(n, BS)), dim3(BS), 0, a, b, n);
 }
@@ -45,13 +32,158 @@ void dev_scale(Dev& d, const double* a, double s, double* b, long long n) {
 void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, long long n) {
   launch(d, k_axpby, dim3(nblocks(n, BS)), dim3(BS), 0, alpha, a, beta, b, n);
 }
-void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n, double* norm) {
-  int parts = red.parts_for(n, 1);
-  launch(d, k_neg_norm, dim3(parts), dim3(BS), 0, n, a, b, red.args(parts, 1, norm), norm);
-}
 
 // ------------------------------------------------------------ FGMRES kernels
-// All take the device scalar block G.  Vectors have length n; V is [(r+1)][n].
+// Grid (parts, owned slices): block (p, y) handles chunk p of the y-th owned slice.  All
+// vectors are in global layout (length n); only owned slices are touched.
+
+__device__ __forceinline__ void seg_chunk(const SegArgs& A, int& s, long long& beg, long long& end) {
+  long long base, l;
+  A.set.slice(blockIdx.y, s, base, l);
+  long long chunk = (l + A.parts - 1) / A.parts;
+  beg = base + (long long)blockIdx.x * chunk;
+  end = base + min(l, (long long)(blockIdx.x + 1) * chunk);
+  if (beg > end) beg = end;
+}
+
+// out[k] = sum over slices s = 0..S-1 (in order) of tot[s][k], k < cnt; all threads of one
+// block; identical code in the fused last block and in the finishing kernel
+__device__ __forceinline__ void seg_total(const SegArgs& A, int cnt, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int S = A.set.S();
+  for (int k = w; k < cnt; k += nw) {
+    double v = 0.0;
+    for (int s = lane; s < S; s += 32) v += __ldcg(A.tot + (size_t)s * GM_NRP + k);
+    v = warp_sum(v);
+    if (lane == 0) out[k] = v;
+  }
+  __syncthreads();
+}
+
+// block partials of cnt values; the last block turns the owned slices' partials into slice
+// totals and (fused) the slice totals into out[0..cnt).  Returns true in every thread of the
+// block that must run the epilogue.
+template <int NR>
+__device__ __forceinline__ bool seg_commit(const double (&acc)[NR], int cnt, const SegArgs& A, int s, double* out) {
+  __shared__ double shn[NR][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NR; k++)
+    if (k < cnt) {
+      double v = warp_sum(acc[k]);
+      if (lane == 0) shn[k][w] = v;
+    }
+  __syncthreads();
+  for (int k = w; k < cnt; k += nw) {
+    double v = lane < nw ? shn[k][lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) {
+      A.partial[((size_t)s * A.parts + blockIdx.x) * GM_NRP + k] = v;
+      __threadfence();
+    }
+  }
+  if (!red_last_block(A.counter)) return false;
+  const int ny = A.set.owned();
+  for (int q = w; q < ny * cnt; q += nw) {
+    int y = q / cnt, k = q - y * cnt;
+    int ss;
+    long long b0, l0;
+    A.set.slice(y, ss, b0, l0);
+    double v = 0.0;
+    for (int p = lane; p < A.parts; p += 32) v += __ldcg(A.partial + ((size_t)ss * A.parts + p) * GM_NRP + k);
+    v = warp_sum(v);
+    if (lane == 0) A.tot[(size_t)ss * GM_NRP + k] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (!A.fused) return false;
+  seg_total(A, cnt, out);
+  return true;
+}
+
+// ---- epilogues (run by one block: the fused last block or the finishing kernel)
+struct EpiResid {      // beta = ||b - op(x)||: start a cycle or stop
+  GmresScal* G;
+  __device__ void operator()(const double* out) const {
+    if (threadIdx.x != 0) return;
+    double beta = sqrt(out[0]);
+    G->beta = beta;
+    G->res = beta;
+    G->j = 0;
+    G->jj = 0;
+    if (!(beta > G->target)) {
+      G->conv = 1;
+      G->flag_inner = 0;
+    } else {
+      G->flag_inner = 1;
+      for (int i = 0; i <= GM_MAXR; i++) G->g[i] = 0.0;
+      G->g[0] = beta;
+    }
+  }
+};
+struct EpiStore {      // h1 / h2 <- the j+1 dots
+  double* dst;
+  int cnt;
+  __device__ void operator()(const double* out) const {
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) dst[k] = out[k];
+  }
+};
+struct EpiNorm {       // *norm = sqrt(sum)
+  double* norm;
+  __device__ void operator()(const double* out) const {
+    if (threadIdx.x == 0) *norm = sqrt(out[0]);
+  }
+};
+struct EpiGivens {     // Hessenberg column, Givens rotations, residual estimate, inner decision (Saad)
+  GmresScal* G;
+  LoopCtl inner;
+  __device__ void operator()(const double* out) const {
+    if (threadIdx.x != 0) return;
+    const int j = G->j;
+    const int r = G->restart;
+    double hn = sqrt(out[0]);
+    double* H = G->H;
+    for (int i = 0; i <= j; i++) H[i * GM_MAXR + j] = G->h1[i] + G->h2[i];
+    H[(j + 1) * GM_MAXR + j] = hn;
+    for (int i = 0; i < j; i++) {
+      double t = G->cs[i] * H[i * GM_MAXR + j] + G->sn[i] * H[(i + 1) * GM_MAXR + j];
+      H[(i + 1) * GM_MAXR + j] = -G->sn[i] * H[i * GM_MAXR + j] + G->cs[i] * H[(i + 1) * GM_MAXR + j];
+      H[i * GM_MAXR + j] = t;
+    }
+    double den = hypot(H[j * GM_MAXR + j], H[(j + 1) * GM_MAXR + j]);
+    G->cs[j] = H[j * GM_MAXR + j] / den;
+    G->sn[j] = H[(j + 1) * GM_MAXR + j] / den;
+    H[j * GM_MAXR + j] = den;
+    H[(j + 1) * GM_MAXR + j] = 0.0;
+    G->g[j + 1] = -G->sn[j] * G->g[j];
+    G->g[j] = G->cs[j] * G->g[j];
+    double res = fabs(G->g[j + 1]);
+    G->res = res;
+    G->jj = j + 1;
+    G->its += 1;
+    G->total_its += 1;
+    G->hn = hn;
+    if (hn <= TINY) G->brk = 1;
+    int cont = !(res <= G->target || G->its >= G->maxit || G->brk) && (j + 1 < r);
+    G->j = j + 1;
+    G->flag_inner = cont;
+    inner.set(cont);
+  }
+};
+
+template <class Epi>
+__global__ void k_seg_finish(SegArgs A, int cnt, Epi epi) {
+  __shared__ double out[GM_NRP];
+  seg_total(A, cnt, out);
+  epi(out);
+}
+// the multi-dot variant: the count j + 1 lives on the device
+__global__ void k_seg_finish_dots(SegArgs A, GmresScal* G, int which) {
+  __shared__ double out[GM_NRP];
+  const int cnt = G->j + 1;
+  seg_total(A, cnt, out);
+  EpiStore{which == 0 ? G->h1 : G->h2, cnt}(out);
+}
 
 __global__ void k_gm_init(GmresScal* G, const double* scale, double tol, int maxit, int restart) {
   G->its = 0;
@@ -67,45 +199,50 @@ __global__ void k_gm_init(GmresScal* G, const double* scale, double tol, int max
   G->flag_inner = 0;
 }
 
-// w = b - w (w = op(x) on entry);  beta = ||w||; start a cycle or stop
-__global__ void k_gm_residual(long long n, const double* __restrict__ b, double* __restrict__ w, GmresScal* G,
-                              RedArgs R) {
+// w = b - w (w = op(x) on entry);  beta = ||w||
+__global__ void k_gm_residual(const double* __restrict__ b, double* __restrict__ w, SegArgs A, EpiResid epi) {
+  int s;
   long long beg, end;
-  red_chunk(n, R.parts, beg, end);
-  double acc = 0.0;
+  seg_chunk(A, s, beg, end);
+  double acc[1] = {0.0};
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double v = b[i] - w[i];
     w[i] = v;
-    acc += v * v;
+    acc[0] += v * v;
   }
-  if (red_commit(acc, R) && threadIdx.x == 0) {
-    double beta = sqrt(R.out[0]);
-    G->beta = beta;
-    G->res = beta;
-    G->j = 0;
-    G->jj = 0;
-    if (!(beta > G->target)) {
-      G->conv = 1;
-      G->flag_inner = 0;
-    } else {
-      G->flag_inner = 1;
-      for (int i = 0; i <= GM_MAXR; i++) G->g[i] = 0.0;
-      G->g[0] = beta;
-    }
+  __shared__ double out[1];
+  if (seg_commit<1>(acc, 1, A, s, out)) epi(out);
+}
+
+// b = -a, ||a||  (inner GMRES right-hand side)
+__global__ void k_gm_neg_norm(const double* __restrict__ a, double* __restrict__ b, SegArgs A, EpiNorm epi) {
+  int s;
+  long long beg, end;
+  seg_chunk(A, s, beg, end);
+  double acc[1] = {0.0};
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = a[i];
+    b[i] = -v;
+    acc[0] += v * v;
   }
+  __shared__ double out[1];
+  if (seg_commit<1>(acc, 1, A, s, out)) epi(out);
 }
 
 // V[j] = w / s and vin = V[j], s = beta (start) or hn (Arnoldi), only if the inner loop continues
 __global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __restrict__ V,
-                           double* __restrict__ vin, const GmresScal* G, int start) {
+                           double* __restrict__ vin, const GmresScal* G, int start, SegArgs A) {
   if (!G->flag_inner) return;
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double s = start ? G->beta : G->hn;
+  int s;
+  long long beg, end;
+  seg_chunk(A, s, beg, end);
+  double sc = start ? G->beta : G->hn;
   int j = start ? 0 : G->j;
-  double v = w[i] / s;
-  V[(size_t)j * n + i] = v;
-  vin[i] = v;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = w[i] / sc;
+    V[(size_t)j * n + i] = v;
+    vin[i] = v;
+  }
 }
 
 // h[k] = V[k] . w for k <= j (one pass over w, one register accumulator per k);
@@ -113,10 +250,11 @@ __global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __
 template <bool COPYZ, int NR>
 __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __restrict__ V,
                                                  const double* __restrict__ w, const double* __restrict__ zout,
-                                                 double* __restrict__ Z, GmresScal* G, int which, RedArgs R) {
+                                                 double* __restrict__ Z, GmresScal* G, SegArgs A) {
   const int j = G->j;
+  int s;
   long long beg, end;
-  red_chunk(n, R.parts, beg, end);
+  seg_chunk(A, s, beg, end);
   double acc[NR];
 #pragma unroll
   for (int k = 0; k < NR; k++) acc[k] = 0.0;
@@ -127,105 +265,72 @@ __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __re
     for (int k = 0; k < NR; k++)
       if (k <= j) acc[k] += V[(size_t)k * n + i] * wi;
   }
-  block_sum_many<NR>(acc, j + 1, R.partial, R.parts);
-  if (!red_last_block(R.counter)) return;
-  double* out = which == 0 ? G->h1 : G->h2;
-  red_finish(R.partial, R.parts, j + 1, out);
+  __shared__ double out[NR];
+  if (seg_commit<NR>(acc, j + 1, A, s, out)) EpiStore{G->h1, j + 1}(out);
 }
 
 // CGS2 middle step in one pass: w -= sum_{k<=j} h1[k] V[k] (first projection),
 // then h2[k] = V[k] . w for the second, reusing the V entries just loaded
 template <int NR>
 __global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double* __restrict__ V,
-                                                      double* __restrict__ w, GmresScal* G, RedArgs R) {
+                                                      double* __restrict__ w, GmresScal* G, SegArgs A) {
   const int j = G->j;
   __shared__ double hs[GM_MAXR + 1];
   if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = G->h1[threadIdx.x];
   __syncthreads();
+  int s;
   long long beg, end;
-  red_chunk(n, R.parts, beg, end);
+  seg_chunk(A, s, beg, end);
   double acc[NR];
 #pragma unroll
   for (int k = 0; k < NR; k++) acc[k] = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double vk[NR];
-    double s = 0.0;
+    double sm = 0.0;
 #pragma unroll
     for (int k = 0; k < NR; k++) {
       vk[k] = 0.0;
       if (k <= j) {
         vk[k] = V[(size_t)k * n + i];
-        s += hs[k] * vk[k];
+        sm += hs[k] * vk[k];
       }
     }
-    double v = w[i] - s;
+    double v = w[i] - sm;
     w[i] = v;
 #pragma unroll
     for (int k = 0; k < NR; k++)
       if (k <= j) acc[k] += vk[k] * v;
   }
-  block_sum_many<NR>(acc, j + 1, R.partial, R.parts);
-  if (!red_last_block(R.counter)) return;
-  red_finish(R.partial, R.parts, j + 1, G->h2);
+  __shared__ double out[NR];
+  if (seg_commit<NR>(acc, j + 1, A, s, out)) EpiStore{G->h2, j + 1}(out);
 }
 
-// w -= sum_{k<=j} h[k] V[k]  (h = h1 or h2); with GIVENS: partial ||w||^2 and,
-// in the last block, the Hessenberg column, Givens rotations, residual estimate
-// and the inner-loop decision (Saad's FGMRES).
-template <bool GIVENS>
+// w -= sum_{k<=j} h2[k] V[k];  ||w|| -> Givens epilogue
 __global__ void __launch_bounds__(256) k_gm_orth(long long n, const double* __restrict__ V, double* __restrict__ w,
-                                                 GmresScal* G, int which, RedArgs R, LoopCtl inner) {
+                                                 GmresScal* G, SegArgs A, EpiGivens epi) {
   const int j = G->j;
-  const double* h = which == 0 ? G->h1 : G->h2;
   __shared__ double hs[GM_MAXR + 1];
-  if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = h[threadIdx.x];
+  if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = G->h2[threadIdx.x];
   __syncthreads();
+  int s;
   long long beg, end;
-  red_chunk(n, R.parts, beg, end);
-  double acc = 0.0;
+  seg_chunk(A, s, beg, end);
+  double acc[1] = {0.0};
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k <= j; k++) s += hs[k] * V[(size_t)k * n + i];
-    double v = w[i] - s;
+    double sm = 0.0;
+    for (int k = 0; k <= j; k++) sm += hs[k] * V[(size_t)k * n + i];
+    double v = w[i] - sm;
     w[i] = v;
-    acc += v * v;
+    acc[0] += v * v;
   }
-  if (!GIVENS) return;
-  if (!red_commit(acc, R) || threadIdx.x != 0) return;
-  const int r = G->restart;
-  double hn = sqrt(R.out[0]);
-  double* H = G->H;
-  for (int i = 0; i <= j; i++) H[i * GM_MAXR + j] = G->h1[i] + G->h2[i];
-  H[(j + 1) * GM_MAXR + j] = hn;
-  for (int i = 0; i < j; i++) {
-    double t = G->cs[i] * H[i * GM_MAXR + j] + G->sn[i] * H[(i + 1) * GM_MAXR + j];
-    H[(i + 1) * GM_MAXR + j] = -G->sn[i] * H[i * GM_MAXR + j] + G->cs[i] * H[(i + 1) * GM_MAXR + j];
-    H[i * GM_MAXR + j] = t;
-  }
-  double den = hypot(H[j * GM_MAXR + j], H[(j + 1) * GM_MAXR + j]);
-  G->cs[j] = H[j * GM_MAXR + j] / den;
-  G->sn[j] = H[(j + 1) * GM_MAXR + j] / den;
-  H[j * GM_MAXR + j] = den;
-  H[(j + 1) * GM_MAXR + j] = 0.0;
-  G->g[j + 1] = -G->sn[j] * G->g[j];
-  G->g[j] = G->cs[j] * G->g[j];
-  double res = fabs(G->g[j + 1]);
-  G->res = res;
-  G->jj = j + 1;
-  G->its += 1;
-  G->total_its += 1;
-  G->hn = hn;
-  if (hn <= TINY) G->brk = 1;
-  int cont = !(res <= G->target || G->its >= G->maxit || G->brk) && (j + 1 < r);
-  G->j = j + 1;
-  G->flag_inner = cont;
-  inner.set(cont);
+  __shared__ double out[1];
+  if (seg_commit<1>(acc, 1, A, s, out)) epi(out);
 }
 
-// x += Z y with y = H^{-1} g (back substitution, redundantly per block); block 0
-// also takes the restart decision for the outer loop.
+// x += Z y with y = H^{-1} g (back substitution, redundantly per block); block (0,0) also
+// takes the restart decision for the outer loop
 __global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __restrict__ Z, double* __restrict__ x,
-                                                   GmresScal* G, LoopCtl outer) {
+                                                   GmresScal* G, LoopCtl outer, SegArgs A) {
   __shared__ double y[GM_MAXR];
   const int jj = G->jj;
   if (threadIdx.x == 0) {
@@ -236,12 +341,15 @@ __global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __
     }
   }
   __syncthreads();
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < jj; k++) s += y[k] * Z[(size_t)k * n + i];
-    if (jj > 0) x[i] += s;
+  int s;
+  long long beg, end;
+  seg_chunk(A, s, beg, end);
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double sm = 0.0;
+    for (int k = 0; k < jj; k++) sm += y[k] * Z[(size_t)k * n + i];
+    if (jj > 0) x[i] += sm;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     if (G->res <= G->target || G->brk) G->conv = 1;
     int cont = !G->conv && G->its < G->maxit;
     G->flag_outer = cont;
@@ -251,8 +359,18 @@ __global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __
 
 __global__ void k_gm_reset_total(GmresScal* G) { G->total_its = 0; }
 
-void DevGmres::ensure(Dev& d, long long n_, int restart_) {
+// parts per slice: a function of the longest slice only (P-invariant), ~2048 values per block
+static int seg_parts(const SliceSet& st) {
+  long long L = st.S_phi > 0 ? st.N : st.nbar;
+  return (int)std::max(1LL, std::min(1024LL, (L + 2047) / 2048));
+}
+
+void DevGmres::ensure(Dev& d, const SliceSet& set_, int restart_, Comm* comm_) {
   if (restart_ > GM_MAXR) throw Error(BBOT_E_INPUT, "restart > 32 not supported");
+  set = set_;
+  comm = comm_;
+  parts = seg_parts(set);
+  const long long n_ = set.len();
   if (n == n_ && restart == restart_ && V.p) return;
   n = n_;
   restart = restart_;
@@ -261,53 +379,84 @@ void DevGmres::ensure(Dev& d, long long n_, int restart_) {
   w.alloc(n, d.stream);
   vin.alloc(n, d.stream);
   zout.alloc(n, d.stream);
+  partial.alloc((size_t)set.S() * parts * GM_NRP, d.stream);
+  tot.alloc((size_t)set.S() * GM_NRP, d.stream);
+  tot.zero();
+  if (!counter.p) {
+    counter.alloc(1, d.stream);
+    counter.zero();
+  }
   if (!sc.p) {
     sc.alloc(1, d.stream);
     BB_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(GmresScal), d.stream));
   }
 }
 
+// the slice totals of every rank to every rank: the potential and the density slices are
+// two slab-partitioned ranges of the [S][GM_NRP] array
+void DevGmres::allgather_tot(Dev& d) {
+  if (set.S_phi > 0) comm->allgather(d, Layout::uniform(set.S_phi, GM_NRP), tot.p);
+  if (set.S_rho > 0) comm->allgather(d, Layout::uniform(set.S_rho, GM_NRP), tot.p + (size_t)set.S_phi * GM_NRP);
+}
+
 void DevGmres::reset_total(Dev& d) { launch(d, k_gm_reset_total, dim3(1), dim3(1), 0, sc.p); }
 
-static int dot_parts_cap() {   // GPU-only tuning knob (env A/B): blocks of the CGS2 multi-dot kernels
-  static const int v = [] { const char* e = getenv("BBOT_DOT_PARTS"); return e ? atoi(e) : 0; }();
-  return v;
+void DevGmres::neg_norm(Dev& d, const double* a, double* b, double* norm) {
+  const bool fused = comm == nullptr;
+  launch(d, k_gm_neg_norm, dim3(parts, set.owned()), dim3(BS), 0, a, b, seg(fused ? 1 : 0), EpiNorm{norm});
+  if (!fused) {
+    allgather_tot(d);
+    launch(d, k_seg_finish<EpiNorm>, dim3(1), dim3(BS), 0, seg(0), 1, EpiNorm{norm});
+  }
 }
 
 void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
                     const double* scale, double tol, int maxit) {
-  const int parts = dot_parts_cap() > 0 ? std::min(red.parts_for(n, 1), dot_parts_cap()) : red.parts_for(n, 1);
-  const unsigned nb = nblocks(n, BS);
-  const unsigned nb_upd = std::min<unsigned>(nb, 8u * d.num_sms);
+  (void)red;
+  const bool fused = comm == nullptr;
+  const dim3 grid(parts, set.owned());
   GmresScal* G = sc.p;
-  double* rout = reinterpret_cast<double*>(dev_field(G, &GmresScal::red_out));
   launch(d, k_gm_init, dim3(1), dim3(1), 0, G, scale, tol, maxit, restart);
   BB_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), d.stream));
+  auto finish = [&](int cnt, auto epi) {
+    if (fused) return;
+    allgather_tot(d);
+    launch(d, k_seg_finish<decltype(epi)>, dim3(1), dim3(BS), 0, seg(0), cnt, epi);
+  };
   dev_while(d, dev_field(G, &GmresScal::flag_outer), [&](const LoopCtl& outer) {
     op(x, w.p);                                               // x = 0 in the first cycle: w = 0 exactly
-    launch(d, k_gm_residual, dim3(parts), dim3(BS), 0, n, b, w.p, G, red.args(parts, 1, rout));
-    launch(d, k_gm_scale, dim3(nb), dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 1);
+    launch(d, k_gm_residual, grid, dim3(BS), 0, b, w.p, seg(fused), EpiResid{G});
+    finish(1, EpiResid{G});
+    launch(d, k_gm_scale, grid, dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 1, seg(fused));
     dev_while(d, dev_field(G, &GmresScal::flag_inner), [&](const LoopCtl& inner) {
       pre(vin.p, zout.p);
       op(zout.p, w.p);
-      // CGS2: two classical Gram-Schmidt passes
+      // CGS2: two classical Gram-Schmidt passes; the dot counts (j + 1) live on the device,
+      // the finishing kernel of the split path reads them from G as well
       if (restart <= 12)
-        launch(d, k_gm_dots<true, 12>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
-               (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
+        launch(d, k_gm_dots<true, 12>, grid, dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+               (const double*)zout.p, Z.p, G, seg(fused));
       else
-        launch(d, k_gm_dots<true, GM_MAXR>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
-               (const double*)zout.p, Z.p, G, 0, red.args(parts, restart + 1, nullptr));
+        launch(d, k_gm_dots<true, GM_MAXR>, grid, dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+               (const double*)zout.p, Z.p, G, seg(fused));
+      if (!fused) {
+        allgather_tot(d);
+        launch(d, k_seg_finish_dots, dim3(1), dim3(BS), 0, seg(0), G, 0);
+      }
       if (restart <= 12)
-        launch(d, k_gm_orth_dots<12>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G,
-               red.args(parts, restart + 1, nullptr));
+        launch(d, k_gm_orth_dots<12>, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused));
       else
-        launch(d, k_gm_orth_dots<GM_MAXR>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G,
-               red.args(parts, restart + 1, nullptr));
-      launch(d, k_gm_orth<true>, dim3(parts), dim3(BS), 0, n, (const double*)V.p, w.p, G, 1,
-             red.args(parts, 1, rout), inner);
-      launch(d, k_gm_scale, dim3(nb), dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0);
+        launch(d, k_gm_orth_dots<GM_MAXR>, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused));
+      if (!fused) {
+        allgather_tot(d);
+        launch(d, k_seg_finish_dots, dim3(1), dim3(BS), 0, seg(0), G, 1);
+      }
+      launch(d, k_gm_orth, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused), EpiGivens{G, inner});
+      finish(1, EpiGivens{G, inner});
+      launch(d, k_gm_scale, grid, dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0,
+             seg(fused));
     });
-    launch(d, k_gm_update, dim3(nb_upd), dim3(BS), 0, n, (const double*)Z.p, x, G, outer);
+    launch(d, k_gm_update, grid, dim3(BS), 0, n, (const double*)Z.p, x, G, outer, seg(fused));
   });
 }
 

@@ -14,6 +14,7 @@
 #pragma once
 #include "common.cuh"
 #include "pcg_fin.cuh"
+#include "comm.cuh"
 #include <functional>
 
 namespace bbot {
@@ -34,19 +35,70 @@ struct GmresScal {
   long long total_its;                  // accumulated over a whole Newton solve (inner T statistic)
 };
 
+// Slice structure of a Krylov vector in global layout: S_phi potential slices of N values,
+// then S_rho density slices of nbar values (FGMRES on (4.17): both; T-GMRES: density only).
+// A rank computes its owned slices: phi [pa, pb), rho [ra, rb) (time slabs, comm.cuh).
+struct SliceSet {
+  long long N = 0, nbar = 0, n_phi = 0;   // n_phi = S_phi * N (offset of the density part)
+  int S_phi = 0, S_rho = 0;
+  int pa = 0, pb = 0, ra = 0, rb = 0;
+  __host__ __device__ int owned() const { return (pb - pa) + (rb - ra); }
+  __host__ __device__ int S() const { return S_phi + S_rho; }
+  __host__ __device__ long long len() const { return n_phi + (long long)S_rho * nbar; }
+  // y-th owned slice -> global slice id s, first element, length
+  __device__ __forceinline__ void slice(int y, int& s, long long& base, long long& l) const {
+    if (y < pb - pa) {
+      s = pa + y;
+      base = (long long)s * N;
+      l = N;
+    } else {
+      int q = ra + (y - (pb - pa));
+      s = S_phi + q;
+      base = n_phi + (long long)q * nbar;
+      l = nbar;
+    }
+  }
+};
+
+// Reductions of a Krylov instance (I6): every dot/norm is the sum over slices,
+// in slice order, of per-slice totals, each the fixed-order sum of `parts` block partials of
+// that slice -- a function of the slice lengths only, so the time-slab decomposition (any P)
+// reproduces the single-GPU bits.  P = 1: the last block finishes the reduction and runs the
+// epilogue in the same launch; P > 1: the slice totals are allgathered and a one-block
+// kernel finishes with the same code.
+constexpr int GM_NRP = GM_MAXR + 1;     // values per slice total (multi-dots)
+struct SegArgs {
+  SliceSet set;
+  int parts;
+  double* partial;      // [S][parts][GM_NRP]
+  double* tot;          // [S][GM_NRP]
+  unsigned* counter;
+  int fused;            // 1: the last block finishes (single rank)
+};
+
 struct DevGmres {
   long long n = 0;
   int restart = 0;
+  SliceSet set;
+  int parts = 1;
+  Comm* comm = nullptr;
   DBuf<double> V, Z, w, vin, zout;     // V [(r+1)][n], Z [r][n]; vin/zout: fixed pre in/out
+  DBuf<double> partial, tot;
+  DBuf<unsigned> counter;
   DBuf<GmresScal> sc;
-  void ensure(Dev& d, long long n_, int restart_);
+  void ensure(Dev& d, const SliceSet& set_, int restart_, Comm* comm_);
+  SegArgs seg(int fused) const { return SegArgs{set, parts, partial.p, tot.p, counter.p, fused}; }
   // Emit: x = FGMRES(op, pre) solution of op x = b from x0 = 0, stopping when the
   // Arnoldi residual <= tol * (*scale) (scale: device scalar).  op / pre are
-  // capture functions (op(in, out), pre(in, out)); pre is always called with
-  // (vin, zout).  Nothing is read back.
+  // capture functions (op(in, out), pre(in, out)) computing the owned slices of `out`
+  // (they exchange the halos they need themselves); pre is always called with (vin, zout).
+  // Nothing is read back.
   void emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, const double* b, double* x,
             const double* scale, double tol, int maxit);
+  // b = -a and *norm = ||a||_2 on this instance's slice set (the inner GMRES right-hand side)
+  void neg_norm(Dev& d, const double* a, double* b, double* norm);
   void reset_total(Dev& d);
+  void allgather_tot(Dev& d);
 };
 
 struct DevPcg {
@@ -75,8 +127,6 @@ struct DevPcg {
 void dev_copy(Dev& d, const double* a, double* b, long long n);
 void dev_scale(Dev& d, const double* a, double s, double* b, long long n);
 void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, long long n);  // b = alpha a + beta b
-// b = -a and *norm = ||a||_2 (one fused launch)
-void dev_neg_norm(Dev& d, Reducer& red, const double* a, double* b, long long n, double* norm);
 
 // r = b, bn = ||b^k||, active = bn > 0, its = 0, it = 0; loop flag = any active
 __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* __restrict__ r, double* s, int* its,

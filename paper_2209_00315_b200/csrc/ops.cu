@@ -26,6 +26,13 @@ __global__ void k_sub_slice(long long L, int ns, double* __restrict__ x, const d
   if (t >= L * ns) return;
   x[t] -= S[t / L] * scale;
 }
+__global__ void k_sub_slice_w_rng(long long L, long long t0, long long t1, double* __restrict__ x,
+                                  const double* __restrict__ w, const double* __restrict__ S, double scale) {
+  long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= t1) return;
+  long long k = t / L;
+  x[t] -= w[t - k * L] * S[k] * scale;
+}
 // x -= w_i S[k] * scale
 __global__ void k_sub_slice_w(long long L, int ns, double* __restrict__ x, const double* __restrict__ w,
                               const double* __restrict__ S, double scale) {
@@ -35,10 +42,32 @@ __global__ void k_sub_slice_w(long long L, int ns, double* __restrict__ x, const
   x[t] -= w[t - k * L] * S[k] * scale;
 }
 
-void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L) {
+__global__ void k_sub_slice_rng(long long L, long long t0, long long t1, double* __restrict__ x,
+                                const double* __restrict__ S, double scale) {
+  long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= t1) return;
+  x[t] -= S[t / L] * scale;
+}
+
+// x -= S[k] * scale on the slices [k0, k1) of a vector of L-value slices (the full-vector
+// launch when they are all of them -- identical values)
+static void sub_slice(bbot_ctx* c, double* x, long long L, int k0, int k1, int ns, const double* S, double scale) {
+  if (k0 == 0 && k1 == ns)
+    launch(c->dev, k_sub_slice, dim3(nblocks(L * ns, BS)), dim3(BS), 0, L, ns, x, S, scale);
+  else if (k1 > k0)
+    launch(c->dev, k_sub_slice_rng, dim3(nblocks(L * (k1 - k0), BS)), dim3(BS), 0, L, k0 * L, k1 * L, x, S, scale);
+}
+
+// slices [k0, k1) of an ns-slice vector: arithmetic mean removed per slice
+static void remove_slice_mean_rng(bbot_ctx* c, double* x, int ns, long long L, int k0, int k1) {
   double* S = c->scal.p;
-  c->red.slice_sum(WSlice{nullptr, x, L}, L, ns, S, false);
-  launch(c->dev, k_sub_slice, dim3(nblocks(L * ns, BS)), dim3(BS), 0, L, ns, x, (const double*)S, 1.0 / (double)L);
+  c->red.slice_sum_range(WSlice{nullptr, x, L}, L, k0, k1, ns, S);
+  sub_slice(c, x, L, k0, k1, ns, S, 1.0 / (double)L);
+}
+
+void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L) {
+  if (ns == c->g.K + 1 && L == c->g.N) remove_slice_mean_rng(c, x, ns, L, c->pa(), c->pb());
+  else remove_slice_mean_rng(c, x, ns, L, 0, ns);
 }
 
 // ---------------------------------------------------------------- B row (coarse)
@@ -115,8 +144,8 @@ static BtRow make_btrow(bbot_ctx* c) {
 // ---------------------------------------------------------------- a2: J_P
 __global__ void k_jp_y1(long long n, int N, const double* __restrict__ Aoff, const int* __restrict__ fnb, BtRow bt,
                         const double* __restrict__ x1, const double* __restrict__ x2, const double* __restrict__ S,
-                        double inv_area, double* __restrict__ y1) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+                        double inv_area, double* __restrict__ y1, long long t0) {
+  long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   int kk = (int)(t / N);
   long long f = t - (long long)kk * N;
@@ -154,10 +183,27 @@ void jp_matvec(bbot_ctx* c, const double* x, double* y) {
   const double* x2 = x + n;
   double* S1 = c->scal.p;            // c-bar weighted slice sums of x2 (P^T)
   double* S2 = c->scal.p + (K + 2);  // plain slice sums of t (P)
+  if (c->slab()) {   // time slabs: one-slice halos of x1 (B, right) and x2 (B^T P^T, left), own rows only
+    Layout Lp = Layout::uniform(K + 1, g.N), Lr = Layout::uniform(K, g.nbar);
+    c->comm->halo(c->dev, Lp, const_cast<double*>(x1));
+    c->comm->halo(c->dev, Lr, const_cast<double*>(x2));
+    const int pa = c->pa(), pb = c->pb(), ra = c->ra(), rb = c->rb();
+    c->red.slice_sum_range(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, std::max(0, ra - 1), rb, K, S1);
+    launch(c->dev, k_jp_y1, dim3(nblocks((long long)(pb - pa) * g.N, BS)), dim3(BS), 0, (long long)pb * g.N, g.N,
+           (const double*)c->as.Aoff.p, (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
+           1.0 / g.area, y, (long long)pa * g.N);
+    c->red.slice_sum_range(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, ra, rb, K,
+                           S2);
+    if (rb > ra)
+      launch(c->dev, k_sub_slice_w_rng, dim3(nblocks((long long)(rb - ra) * g.nbar, BS)), dim3(BS), 0,
+             (long long)g.nbar, (long long)ra * g.nbar, (long long)rb * g.nbar, y + n, (const double*)g.cbar.p,
+             (const double*)S2, 1.0 / g.area);
+    return;
+  }
   c->red.slice_sum(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, K, S1, false);
   launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)c->as.Aoff.p,
          (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
-         1.0 / g.area, y);
+         1.0 / g.area, y, 0LL);
   c->red.slice_sum(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, K, S2, false);
   launch(c->dev, k_sub_slice_w, dim3(nblocks(m, BS)), dim3(BS), 0, (long long)g.nbar, K, y + n,
          (const double*)g.cbar.p, (const double*)S2, 1.0 / g.area);
@@ -177,7 +223,7 @@ void j_matvec(bbot_ctx* c, const double* x, double* y) {
   DevGeom& g = c->g;
   long long n = c->n(), m = c->m();
   launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)c->as.Aoff.p,
-         (const int*)g.fadj_nb.p, make_btrow(c), x, x + n, (const double*)nullptr, 0.0, y);
+         (const int*)g.fadj_nb.p, make_btrow(c), x, x + n, (const double*)nullptr, 0.0, y, 0LL);
   launch(c->dev, k_j_y2, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, make_brow(c), x, x + n,
          (const double*)c->as.Cd.p, y + n);
 }
@@ -272,9 +318,9 @@ void hss_out(bbot_ctx* c, const double* v, double* z) {
 
 // ---------------------------------------------------------------- y = T x, y = A x
 template <class V>
-__global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y) {
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= v.nrows) return;
+__global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y, long long r0, long long r1) {
+  long long r = r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
   double acc = 0.0;
   v.row(r, [&](long long col, double a) { acc += a * x[col]; });
   y[r] = acc;
@@ -282,11 +328,17 @@ __global__ void k_spmv(V v, const double* __restrict__ x, double* __restrict__ y
 
 void apply_T(bbot_ctx* c, const double* x, double* y) {
   SliceEllView v = view_T(c);
-  launch(c->dev, k_spmv<SliceEllView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
+  if (c->slab()) {   // time slabs: z halos from both neighbours (T is block tridiagonal in time), own rows
+    c->comm->halo(c->dev, Layout::uniform(c->g.K, c->g.nbar), const_cast<double*>(x));
+    long long r0 = (long long)c->ra() * c->g.nbar, r1 = (long long)c->rb() * c->g.nbar;
+    launch(c->dev, k_spmv<SliceEllView>, dim3(nblocks(std::max(1LL, r1 - r0), BS)), dim3(BS), 0, v, x, y, r0, r1);
+    return;
+  }
+  launch(c->dev, k_spmv<SliceEllView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y, 0LL, v.nrows);
 }
 void apply_A(bbot_ctx* c, const double* x, double* y) {
   LapView v = view_A(c);
-  launch(c->dev, k_spmv<LapView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y);
+  launch(c->dev, k_spmv<LapView>, dim3(nblocks(v.nrows, BS)), dim3(BS), 0, v, x, y, 0LL, v.nrows);
 }
 
 // ---------------------------------------------------------------- a4 pieces
@@ -309,13 +361,12 @@ struct AtZ {   // v = (Atilde_k z)_i / cbar_i, stored; returns cbar_i v (for P^T
   }
 };
 
-void bb_y_from_z(bbot_ctx* c, const double* z, double* y) {
+void bb_y_from_z(bbot_ctx* c, const double* z, double* y) {   // per density slice: the slab's own slices
   DevGeom& g = c->g;
   double* S = c->scal.p;
-  c->red.slice_sum(AtZ{g.nbar, g.NEbar, z, c->as.omegabar.p, g.cbar.p, g.cadj_e.p, g.cadj_nb.p, y}, g.nbar, g.K, S,
-                   false);
-  launch(c->dev, k_sub_slice, dim3(nblocks(c->m(), BS)), dim3(BS), 0, (long long)g.nbar, g.K, y, (const double*)S,
-         1.0 / g.area);
+  c->red.slice_sum_range(AtZ{g.nbar, g.NEbar, z, c->as.omegabar.p, g.cbar.p, g.cadj_e.p, g.cadj_nb.p, y}, g.nbar,
+                         c->ra(), c->rb(), g.K, S);
+  sub_slice(c, y, g.nbar, c->ra(), c->rb(), g.K, S, 1.0 / g.area);
 }
 
 struct RhsA {  // b = r1 - B^T y, stored; returns b
@@ -334,9 +385,9 @@ struct RhsA {  // b = r1 - B^T y, stored; returns b
 void bb_rhs_A(bbot_ctx* c, const double* r1, const double* y, double* b) {
   DevGeom& g = c->g;
   double* S = c->scal.p;
-  c->red.slice_sum(RhsA{make_btrow(c), r1, y, b, g.N}, g.N, g.K + 1, S, false);
-  launch(c->dev, k_sub_slice, dim3(nblocks(c->n(), BS)), dim3(BS), 0, (long long)g.N, g.K + 1, b, (const double*)S,
-         1.0 / (double)g.N);
+  if (c->slab()) c->comm->halo(c->dev, Layout::uniform(g.K, g.nbar), const_cast<double*>(y));   // B^T: y^{k-1}
+  c->red.slice_sum_range(RhsA{make_btrow(c), r1, y, b, g.N}, g.N, c->pa(), c->pb(), g.K + 1, S);
+  sub_slice(c, b, g.N, c->pa(), c->pb(), g.K + 1, S, 1.0 / (double)g.N);
 }
 
 // ---------------------------------------------------------------- solve(rhs)
@@ -455,17 +506,51 @@ __global__ void k_prefix_shift(int K, double dt, double inv_area, const double* 
 }
 
 __global__ void k_add_shift(long long n, int N, const double* __restrict__ src, const double* __restrict__ shift,
-                            double* __restrict__ dst) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+                            double* __restrict__ dst, long long t0) {
+  long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   dst[t] = src[t] + shift[t / N];
 }
 
 __global__ void k_ds(long long m, const double* __restrict__ h, const double* __restrict__ s,
-                     const double* __restrict__ drho, const double* __restrict__ rho, double* __restrict__ ds) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+                     const double* __restrict__ drho, const double* __restrict__ rho, double* __restrict__ ds,
+                     long long t0) {
+  long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m) return;
   ds[t] = (h[t] - s[t] * drho[t]) / rho[t];
+}
+
+// a6 on a time slab: the same steps on the rank's own slices; B dphit needs the right
+// dphit halo, the time prefix of dlambda all K slice sums (allgathered, then summed in
+// order on every rank); the direction is then allgathered for the replicated update (a7)
+static void recover_slab(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  long long n = c->n(), m = c->m();
+  int K = g.K;
+  cudaStream_t s = c->dev.stream;
+  const int pa = c->pa(), pb = c->pb(), ra = c->ra(), rb = c->rb();
+  double* S = c->scal.p;
+  double* shift = c->scal.p + 2 * (K + 2);
+  BB_CUDA(cudaMemcpyAsync(c->drho.p, c->sol.p + n, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  c->red.slice_sum_range(WSlice{g.cbar.p, c->drho.p, g.nbar}, g.nbar, ra, rb, K, S);
+  sub_slice(c, c->drho.p, g.nbar, ra, rb, K, S, 1.0 / g.area);
+  double* dphit = c->tmp_n.p;
+  BB_CUDA(cudaMemcpyAsync(dphit, c->sol.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  c->red.slice_sum_range(WSlice{g.c.p, dphit, g.N}, g.N, pa, pb, K + 1, S);
+  sub_slice(c, dphit, g.N, pa, pb, K + 1, S, 1.0 / g.area);
+  c->comm->halo(c->dev, Layout::uniform(K + 1, g.N), dphit);
+  c->red.slice_sum_range(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar}, g.nbar, ra, rb, K, S);
+  c->comm->allgather(c->dev, Layout::uniform(K, 1), S);
+  launch(c->dev, k_prefix_shift, dim3(1), dim3(32), 0, K, g.dt, 1.0 / g.area, (const double*)S, shift);
+  launch(c->dev, k_add_shift, dim3(nblocks((long long)(pb - pa) * g.N, BS)), dim3(BS), 0, (long long)pb * g.N, g.N,
+         (const double*)dphit, (const double*)shift, c->dphi.p, (long long)pa * g.N);
+  if (rb > ra)
+    launch(c->dev, k_ds, dim3(nblocks((long long)(rb - ra) * g.nbar, BS)), dim3(BS), 0, (long long)rb * g.nbar,
+           (const double*)c->as.h.p, (const double*)c->s.p, (const double*)c->drho.p,
+           (const double*)(c->rho_ext.p + g.nbar), c->ds.p, (long long)ra * g.nbar);
+  c->comm->allgather(c->dev, Layout::uniform(K + 1, g.N), c->dphi.p);
+  c->comm->allgather(c->dev, Layout::uniform(K, g.nbar), c->drho.p);
+  c->comm->allgather(c->dev, Layout::uniform(K, g.nbar), c->ds.p);
 }
 
 void recover(bbot_ctx* c) {
@@ -477,7 +562,11 @@ void recover(bbot_ctx* c) {
     BB_CUDA(cudaMemcpyAsync(c->dphi.p, c->sol.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     BB_CUDA(cudaMemcpyAsync(c->drho.p, c->sol.p + n, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
     launch(c->dev, k_ds, dim3(nblocks(m, BS)), dim3(BS), 0, m, (const double*)c->as.h.p, (const double*)c->s.p,
-           (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p);
+           (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p, 0LL);
+    return;
+  }
+  if (c->slab()) {
+    recover_slab(c);
     return;
   }
   double* S = c->scal.p;
@@ -497,9 +586,9 @@ void recover(bbot_ctx* c) {
   c->red.slice_sum(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar}, g.nbar, K, S, false);
   launch(c->dev, k_prefix_shift, dim3(1), dim3(32), 0, K, g.dt, 1.0 / g.area, (const double*)S, shift);
   launch(c->dev, k_add_shift, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)dphit, (const double*)shift,
-         c->dphi.p);
+         c->dphi.p, 0LL);
   launch(c->dev, k_ds, dim3(nblocks(m, BS)), dim3(BS), 0, m, (const double*)c->as.h.p, (const double*)c->s.p,
-         (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p);
+         (const double*)c->drho.p, (const double*)(c->rho_ext.p + g.nbar), c->ds.p, 0LL);
 }
 
 // ---------------------------------------------------------------- a7 update

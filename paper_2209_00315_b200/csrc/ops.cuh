@@ -41,10 +41,8 @@ void solve(bbot_ctx* c, bbot_solve_stats* st);                                  
 void drop_solve_graph(bbot_ctx* c);
 
 // dist.cu
-int slab_begin(int nslices, int rank, int nranks);
 void nccl_unique_id(unsigned char out[128]);
-void set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid);
+void set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid, long long group);
 void drop_dist(bbot_ctx* c);
-void exchange_slabs(bbot_ctx* c, double* x);   // every rank's slab of [K+1][N] to every rank
 
 }  // namespace bbot

@@ -124,8 +124,24 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
 static void prepare(bbot_ctx* c) {
   const bbot_solver_opts& o = c->opts;
   long long n = c->n(), m = c->m();
-  c->outer.ensure(c->dev, n + m, o.restart);
-  c->innerT.ensure(c->dev, m, o.restart_T);
+  BB_REQUIRE(!c->slab() || c->as.precond == 0, BBOT_E_INPUT, "time slabs: BB preconditioner only (precond 0)");
+  // slice structure of the Krylov vectors and the owned slices (time slabs, comm.cuh)
+  SliceSet so;
+  so.N = c->g.N;
+  so.nbar = c->g.nbar;
+  so.n_phi = n;
+  so.S_phi = c->g.K + 1;
+  so.S_rho = c->g.K;
+  so.pa = c->pa();
+  so.pb = c->pb();
+  so.ra = c->ra();
+  so.rb = c->rb();
+  SliceSet st = so;
+  st.S_phi = 0;
+  st.n_phi = 0;
+  st.pa = st.pb = 0;
+  c->outer.ensure(c->dev, so, o.restart, c->comm.get());
+  c->innerT.ensure(c->dev, st, o.restart_T, c->comm.get());
   c->pcg.ensure(c->dev, n, c->g.K + 1);
   if (!c->nrm_T.p) c->nrm_T.alloc(4, c->dev.stream);
 }
@@ -139,12 +155,16 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   double* z1 = z;
   double* z2 = z + n;
   // (i) T z2 = -r2, GMRES(restart_T) right-preconditioned by one AMG(T) V-cycle, relative eps_T
-  dev_neg_norm(c->dev, c->red, r2, c->tmp_m.p, m, c->nrm_T.p);
+  (void)m;
+  c->innerT.neg_norm(c->dev, r2, c->tmp_m.p, c->nrm_T.p);
   SliceEllView vT = view_T(c);
   c->innerT.emit(
       c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
-      [&](const double* x, double* y) { amg_vcycle(c->dev, c->amgT, vT, x, y); }, c->tmp_m.p, c->tmp_m2.p,
-      c->nrm_T.p, o.eps_T, o.maxit_inner);
+      [&](const double* x, double* y) {
+        if (c->slab()) amg_vcycle_slab(c->dev, c->amgT, vT, x, y, *c->comm, c->ra(), c->rb());
+        else amg_vcycle(c->dev, c->amgT, vT, x, y);
+      },
+      c->tmp_m.p, c->tmp_m2.p, c->nrm_T.p, o.eps_T, o.maxit_inner);
   // (ii) y = P^T Mbar^-1 Atilde z   (A12)
   bb_y_from_z(c, c->tmp_m2.p, z2);
   // (iii) b = r1 - B^T P^T y, slice means removed (compatibility)
@@ -157,8 +177,7 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
         return amg_vcycle(c->dev, c->amgA, vA, x, y, f, f ? f->active : nullptr);
       },
       c->tmp_n2.p, z1, c->g.N, o.eps_A, o.maxit_inner, c->own_begin, c->own_end);
-  exchange_slabs(c, z1);        // multi-GPU: every rank's A_k solutions to every rank (dist.cu)
-  remove_slice_mean(c, z1, c->g.K + 1, c->g.N);
+  remove_slice_mean(c, z1, c->g.K + 1, c->g.N);   // (own slices)
 }
 
 // NEXT f1: z = SIMPLE(r) (eq:sca-precs; oracle/simple.py):
@@ -167,8 +186,9 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
 static void emit_simple_apply(bbot_ctx* c, const double* r, double* z) {
   const bbot_solver_opts& o = c->opts;
   long long m = c->m();
+  (void)m;
   simple_c(c, r, c->tmp_n2.p, c->tmp_m2.p);
-  dev_neg_norm(c->dev, c->red, c->tmp_m2.p, c->tmp_m.p, m, c->nrm_T.p);
+  c->innerT.neg_norm(c->dev, c->tmp_m2.p, c->tmp_m.p, c->nrm_T.p);
   SliceEllView vS = view_T(c);
   c->innerT.emit(
       c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
@@ -184,8 +204,9 @@ static void emit_simple_apply(bbot_ctx* c, const double* r, double* z) {
 static void emit_hss_apply(bbot_ctx* c, const double* r, double* z) {
   const bbot_solver_opts& o = c->opts;
   long long m = c->m();
+  (void)m;
   hss_c(c, r, c->tmp_m2.p);
-  dev_neg_norm(c->dev, c->red, c->tmp_m2.p, c->tmp_m.p, m, c->nrm_T.p);
+  c->innerT.neg_norm(c->dev, c->tmp_m2.p, c->tmp_m.p, c->nrm_T.p);
   SliceEllView vS = view_T(c);
   c->innerT.emit(
       c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
@@ -229,8 +250,9 @@ static void emit_solve(bbot_ctx* c) {
 template <class Emit>
 static void run_emitted(bbot_ctx* c, cudaGraphExec_t* cache, Emit&& emit) {
   Dev& d = c->dev;
-  // NCCL inside conditional-node graphs is not relied on: multi-rank solves run eagerly
-  bool graph = c->use_graph && !d.prof && cache != nullptr && c->comm == nullptr;
+  // the exchanges of a multi-rank solve are host-fenced (virtual ranks) or NCCL calls between
+  // host-driven loop iterations: multi-rank solves run eagerly
+  bool graph = c->use_graph && !d.prof && cache != nullptr && !c->slab();
   c->t_capture_ms = 0;
   if (!graph) {
     emit();

@@ -130,31 +130,3 @@ def test_C3_direction_satisfies_newton_system():
     assert abs(d.M @ dphi[:d.N]) <= 1e-10 * np.abs(dphi).max() * d.M.sum()
 
 
-def test_time_slab_partition_virtual_ranks():
-    """Multi-GPU time slabs on one GPU: P = 3 virtual ranks each
-    solve the A_k systems of their own slab only (no communication); stitched
-    together, their BB-apply outputs equal the single-GPU output bitwise -- what
-    the NCCL exchange assembles on every rank in a multi-GPU run."""
-    pb = _gpu()
-    p = make_problem("C1")
-    phi, rho, s = random_state(p, seed=5, mu=1e-2)
-    r = np.random.default_rng(9).standard_normal(p.n + p.m)
-    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
-    r[p.n:] = d.P(r[p.n:])
-    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
-    ctx.set_state(phi, rho, s, 1e-2)
-    ctx.assemble()
-    z, _, _ = ctx.bb_apply(r)
-    P, N = 3, d.N
-    stitched = np.full_like(z, np.nan)
-    for rank in range(P):
-        c = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
-        c.set_dist(rank, P, None)
-        a, b = c.slab()
-        assert (a, b) == (rank * (p.K + 1) // P, (rank + 1) * (p.K + 1) // P)
-        c.set_state(phi, rho, s, 1e-2)
-        c.assemble()
-        zr, _, _ = c.bb_apply(r)
-        stitched[a * N:b * N] = zr[a * N:b * N]
-        assert np.array_equal(zr[p.n:], z[p.n:])          # the replicated part
-    assert np.array_equal(stitched[:p.n], z[:p.n])
