@@ -1,7 +1,8 @@
-"""Write tests/golden/oracle_counts.json: the oracle's own FGMRES outer-iteration
-counts on the bench systems (calls only oracle/ and synthetic/).  Used by
-bench.py to scale the bounded oracle sample (setup + 3 outer iterations) to a
-full Newton solve for the cpu_baseline / reference arm."""
+"""Write tests/golden/oracle_counts.json: the oracle's own FGMRES outer-iteration and
+inner counts on the first IPM Newton system (A19 point, mu = 1) of the configs (calls only
+oracle/ and synthetic/, one core).  The GPU parity tests hold the CUDA path to these counts
+(+-1 outer) on the configs too large to re-run the oracle inside a test (C2: ~1 min, C3:
+~15 min on one core)."""
 import json
 import os
 import sys
@@ -30,7 +31,9 @@ def main(names):
             S.solve()
         key = f"{name}/init/mu=1"
         data[key] = dict(outer_its=S.stats["outer_its"], inner_T_its=S.stats["inner_T_its"],
-                         converged=S.stats["converged"], seconds_1core=round(time.time() - t, 1))
+                         inner_A_its_max=S.stats["inner_A_its_max"], inner_A_its_total=S.stats["inner_A_its_total"],
+                         converged=S.stats["converged"], rel_res=float(S.stats["rel_res"]),
+                         seconds_1core=round(time.time() - t, 1))
         print(key, data[key], flush=True)
         json.dump(data, open(OUT, "w"), indent=1, sort_keys=True)
 

@@ -128,5 +128,13 @@ def test_C3_direction_satisfies_newton_system():
     assert np.linalg.norm(res) <= 1e-8 * np.linalg.norm(rhs), np.linalg.norm(res) / np.linalg.norm(rhs)
     # kernel of J (Remark 3.1): the gauge fixes delta phi^1 to zero c-weighted mean (A11)
     assert abs(d.M @ dphi[:d.N]) <= 1e-10 * np.abs(dphi).max() * d.M.sum()
+    # north star counts: the oracle's own solve of this system (scripts/oracle_counts.py, oracle
+    # only, ~15 min on one core; tests/golden/oracle_counts.json)
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_counts.json")))
+    o = gold.get("C3/init/mu=1")
+    if o is not None:
+        assert o["converged"] and abs(st["outer_its"] - o["outer_its"]) <= 1, (st, o)
 
 
