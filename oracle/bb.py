@@ -146,7 +146,8 @@ class BBSolver:
         drho = d.PT(sol[n:])                                             # A30
         dphit = dphit - (dphit @ d.M)[:, None] / d.area                  # A11
         dphit = dphit.reshape(-1)
-        q = (self.gt - self.B @ dphit + self.C * drho).reshape(K, d.nbar)
+        Cd = self.C @ drho if d.recon == "harm" else self.C * drho        # C_H δρ (Remark 3.3)
+        q = (self.gt - self.B @ dphit + Cd).reshape(K, d.nbar)
         dlam = q.sum(axis=1) / d.area
         shift = np.concatenate([[0.0], np.cumsum(d.dt * dlam)])          # Σ_{i<k} Δt δλ^i (A10)
         dphi = (dphit.reshape(K + 1, N) + shift[:, None]).reshape(-1)

@@ -58,6 +58,7 @@ class HssSolver:
         self.f, self.g, self.h, self.gt = d.newton_rhs(phi, rho, s, mu)
         self.scale = float(np.sqrt(self.f @ self.f + self.g @ self.g + self.h @ self.h))
         self.rhs = np.concatenate([self.f, self.gt])
+        assert d.recon == "arith", "HSS: arithmetic reconstruction only (the harmonic R_H is built for BB)"
         self.A = d.A(rho)
         self.B = d.B(phi)
         self.BT = self.B.T.tocsr()
