@@ -129,7 +129,7 @@ class BBSolver:
         mk = -d.dt * np.cumsum(Sf)[:K]                                    # m_1 .. m_K
         drho0 = np.repeat(mk / d.area, d.nbar)
         self.f = f - self.BT @ drho0
-        self.g = g
+        self.g = g - d.W(self.phi, self.rho) @ drho0 if d.recon == "harm" else g     # W δρ₀ (f4)
         self.h = h - self.s * drho0
         self.gt = self.g - np.tile(d.Mbar, K) * self.h / self.rho         # g̃
         self.scale = float(np.sqrt(f @ f + g @ g + h @ h))

@@ -26,7 +26,8 @@ class SolverOpts(C.Structure):
                 ("maxit_inner", C.c_int), ("omega_A", C.c_double), ("omega_T", C.c_double),
                 ("coarse_max_A", C.c_int), ("coarse_max_T", C.c_int),
                 ("precond", C.c_int), ("coarse_max_S", C.c_int),   # 0 = BB, 1 = SIMPLE (NEXT f1), 2 = HSS (f2)
-                ("alpha_hss", C.c_double), ("eps_in_hss", C.c_double)]
+                ("alpha_hss", C.c_double), ("eps_in_hss", C.c_double),
+                ("recon", C.c_int)]                                # 0 = arithmetic, 1 = harmonic (f4)
 
 
 class SolveStats(C.Structure):

@@ -214,7 +214,8 @@ SliceEllView view_T(bbot_ctx* c) {
 __global__ void k_edges(int K, int N, int NE, int nbar, const int* __restrict__ eL, const int* __restrict__ eR,
                         const double* __restrict__ lam, const double* __restrict__ e_len,
                         const double* __restrict__ w_len, const double* __restrict__ phi,
-                        const double* __restrict__ rho_ext, double* __restrict__ omega, double* __restrict__ gphi) {
+                        const double* __restrict__ rho_ext, double* __restrict__ omega, double* __restrict__ gphi,
+                        int harm) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)(K + 1) * NE) return;
   int kk = (int)(t / NE);
@@ -224,7 +225,7 @@ __global__ void k_edges(int K, int N, int NE, int nbar, const int* __restrict__ 
   const double* ra = rho_ext + (size_t)(kk + 1) * nbar;   // rho^k   (k = kk+1, 1-based)
   const double* rb = rho_ext + (size_t)kk * nbar;         // rho^{k-1}
   double l = lam[e];
-  double rt = l * (0.5 * (ra[pL] + rb[pL])) + (1.0 - l) * (0.5 * (ra[pR] + rb[pR]));
+  double rt = Recon::eval(harm, l, 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR])).f;   // R_E or R_H
   double wl = w_len[e];
   omega[t] = e_len[e] * rt / wl;
   gphi[t] = (phi[(size_t)kk * N + L] - phi[(size_t)kk * N + R]) / wl;
@@ -248,14 +249,45 @@ __global__ void k_cell_lap(long long n, int N, int NE, const int* __restrict__ f
 
 __global__ void k_coarse_edges(int K, int NEbar, int nbar, const int* __restrict__ ebL, const int* __restrict__ ebR,
                                const double* __restrict__ lam_bar, const double* __restrict__ ebar_coef,
-                               const double* __restrict__ rho_ext, double* __restrict__ omegabar) {
+                               const double* __restrict__ rho_ext, double* __restrict__ omegabar, int harm) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)K * NEbar) return;
   int k0 = (int)(t / NEbar);
   int e = (int)(t - (long long)k0 * NEbar);
   const double* r = rho_ext + (size_t)(k0 + 1) * nbar;
   double l = lam_bar[e];
-  omegabar[t] = ebar_coef[e] * (l * r[ebL[e]] + (1.0 - l) * r[ebR[e]]);
+  omegabar[t] = ebar_coef[e] * Recon::eval(harm, l, r[ebL[e]], r[ebR[e]]).f;   // R-bar (A35) or R-bar_H (A40)
+}
+
+// harmonic reconstruction (NEXT f4): sr = diag(C_H) / cbar = (C - diag W) / cbar, the diagonal
+// the BB preconditioner uses in T (Remark 3.3); diag W at row (k0, i) =
+// 1/8 sum over phi slices kk = k0, k0+1 of sum_{sigma in E(i), two parents} D (g^kk)^2 h_ii
+__global__ void k_harm_sr(long long m, int nbar, int NE, const int* __restrict__ ce_edge,
+                          const int* __restrict__ eL, const int* __restrict__ eR, const double* __restrict__ lam,
+                          const double* __restrict__ e_len, const double* __restrict__ w_len,
+                          const double* __restrict__ gphi, const double* __restrict__ rho_ext,
+                          const double* __restrict__ cbar, const double* __restrict__ Cd, double* __restrict__ sr) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  int i = (int)(t - (long long)k0 * nbar);
+  double wd = 0.0;
+  for (int side = 0; side < 2; side++) {
+    int kk = k0 + side;
+    const double* ra = rho_ext + (size_t)(kk + 1) * nbar;
+    const double* rb = rho_ext + (size_t)kk * nbar;
+    const double* gk = gphi + (size_t)kk * NE;
+    for (int q = 0; q < CE_MAX; q++) {
+      int e = ce_edge[(size_t)q * nbar + i];
+      if (e < 0) break;
+      int pL = eL[e] / 3, pR = eR[e] / 3;
+      if (pL == pR) continue;             // one parent: R_H is linear there
+      double haa, hab, hbb;
+      Recon::hess(lam[e], 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR]), haa, hab, hbb);
+      wd += w_len[e] * e_len[e] * gk[e] * gk[e] * (pL == i ? haa : hbb);
+    }
+  }
+  sr[t] = (Cd[t] - 0.125 * wd) / cbar[i];
 }
 
 __global__ void k_cdiag(long long m, int nbar, const double* __restrict__ cbar, const double* __restrict__ s,
@@ -281,17 +313,23 @@ void assemble_edges(bbot_ctx* c) {
     A.Cd.alloc(c->m(), s);
     A.sr.alloc(c->m(), s);
   }
+  const int harm = c->opts.recon;
   launch(c->dev, k_edges, dim3(nblocks(ne, BS)), dim3(BS), 0, g.K, g.N, g.NE, g.nbar, (const int*)g.eL.p,
          (const int*)g.eR.p, (const double*)g.lam.p, (const double*)g.e_len.p, (const double*)g.w_len.p,
-         (const double*)c->phi.p, (const double*)c->rho_ext.p, A.omega.p, A.gphi.p);
+         (const double*)c->phi.p, (const double*)c->rho_ext.p, A.omega.p, A.gphi.p, harm);
   launch(c->dev, k_cell_lap, dim3(nblocks(c->n(), BS)), dim3(BS), 0, c->n(), g.N, g.NE, (const int*)g.fadj_e.p,
          (const double*)A.omega.p, A.Aoff.p);
   long long nce = (long long)g.K * g.NEbar;
   launch(c->dev, k_coarse_edges, dim3(nblocks(nce, BS)), dim3(BS), 0, g.K, g.NEbar, g.nbar, (const int*)g.ebL.p,
          (const int*)g.ebR.p, (const double*)g.lam_bar.p, (const double*)g.ebar_coef.p,
-         (const double*)c->rho_ext.p, A.omegabar.p);
+         (const double*)c->rho_ext.p, A.omegabar.p, harm);
   launch(c->dev, k_cdiag, dim3(nblocks(c->m(), BS)), dim3(BS), 0, c->m(), g.nbar, (const double*)g.cbar.p,
          (const double*)c->s.p, (const double*)c->rho_ext.p, A.Cd.p, A.sr.p);
+  if (harm)
+    launch(c->dev, k_harm_sr, dim3(nblocks(c->m(), BS)), dim3(BS), 0, c->m(), g.nbar, g.NE, (const int*)g.ce_edge.p,
+           (const int*)g.eL.p, (const int*)g.eR.p, (const double*)g.lam.p, (const double*)g.e_len.p,
+           (const double*)g.w_len.p, (const double*)A.gphi.p, (const double*)c->rho_ext.p,
+           (const double*)g.cbar.p, (const double*)A.Cd.p, A.sr.p);
 }
 
 // ---------------------------------------------------------------- residuals
@@ -325,6 +363,9 @@ struct FRhoF {
   const double *cf, *cbar, *phi, *gphi, *s, *rho_ext, *ce_coef, *e_len, *w_len;
   const int* ce_edge;
   double *g, *h, *gt;
+  int harm;
+  const int *eL, *eR;
+  const double* lam;
   __device__ double operator()(int k0, long long i) const {
     const double* p0 = phi + (size_t)k0 * N;
     const double* p1 = phi + (size_t)(k0 + 1) * N;
@@ -336,10 +377,26 @@ struct FRhoF {
     const double* g0 = gphi + (size_t)k0 * NE;
     const double* g1 = gphi + (size_t)(k0 + 1) * NE;
     double dr = 0.0;
-    for (int q = 0; q < CE_MAX; q++) {
-      int e = ce_edge[(size_t)q * nbar + i];
-      if (e < 0) break;
-      dr += ce_coef[(size_t)q * nbar + i] * w_len[e] * e_len[e] * (g0[e] * g0[e] + g1[e] * g1[e]);
+    if (!harm) {
+      for (int q = 0; q < CE_MAX; q++) {
+        int e = ce_edge[(size_t)q * nbar + i];
+        if (e < 0) break;
+        dr += ce_coef[(size_t)q * nbar + i] * w_len[e] * e_len[e] * (g0[e] * g0[e] + g1[e] * g1[e]);
+      }
+    } else {    // 1/4 [J(rho-bar^k)^T D (g^k)^2 + J(rho-bar^{k+1})^T D (g^{k+1})^2]  (f4)
+      const double* r0 = rho_ext + (size_t)k0 * nbar;
+      const double* r1 = rho_ext + (size_t)(k0 + 1) * nbar;
+      const double* r2 = rho_ext + (size_t)(k0 + 2) * nbar;
+      for (int q = 0; q < CE_MAX; q++) {
+        int e = ce_edge[(size_t)q * nbar + i];
+        if (e < 0) break;
+        int pL = eL[e] / 3, pR = eR[e] / 3;
+        Recon a = Recon::eval(1, lam[e], 0.5 * (r1[pL] + r0[pL]), 0.5 * (r1[pR] + r0[pR]));
+        Recon b = Recon::eval(1, lam[e], 0.5 * (r2[pL] + r1[pL]), 0.5 * (r2[pR] + r1[pR]));
+        double ja = (pL == i ? a.ja : 0.0) + (pR == i ? a.jb : 0.0);
+        double jb = (pL == i ? b.ja : 0.0) + (pR == i ? b.jb : 0.0);
+        dr += w_len[e] * e_len[e] * (ja * g0[e] * g0[e] + jb * g1[e] * g1[e]);
+      }
     }
     size_t t = (size_t)k0 * nbar + i;
     double si = s[t], ri = rho_ext[nbar + t];
@@ -387,7 +444,8 @@ void compute_residual(bbot_ctx* c, bool write_rhs) {
                          A.f.p},
                    g.N, K + 1, sc, false);
   c->red.slice_sum(FRhoF{g.N, g.NE, g.nbar, g.dt, c->mu, g.c.p, g.cbar.p, c->phi.p, A.gphi.p, c->s.p, c->rho_ext.p,
-                         g.ce_coef.p, g.e_len.p, g.w_len.p, g.ce_edge.p, A.g.p, A.h.p, A.gt.p},
+                         g.ce_coef.p, g.e_len.p, g.w_len.p, g.ce_edge.p, A.g.p, A.h.p, A.gt.p, c->opts.recon, g.eL.p,
+                         g.eR.p, g.lam.p},
                    g.nbar, K, sc + K + 1, false);
   std::vector<double> hs(2 * K + 1);
   if (write_rhs) {
@@ -417,7 +475,9 @@ __global__ void __launch_bounds__(128) k_assemble_T(
     const int* __restrict__ cadj_e, const int* __restrict__ ca_pos, const int* __restrict__ fi_cell,
     const int* __restrict__ fi_child, const int* __restrict__ fi_ppos, const int* __restrict__ fi_edge,
     const double* __restrict__ fi_alpha, const int* __restrict__ fi_tbe, const double* __restrict__ fi_tbbeta,
-    const int* __restrict__ fi_tbpL, const int* __restrict__ fi_tbpR, double* __restrict__ Tv) {
+    const int* __restrict__ fi_tbpL, const int* __restrict__ fi_tbpR, double* __restrict__ Tv, int harm,
+    const int* __restrict__ eL, const int* __restrict__ eR, const double* __restrict__ lam,
+    const double* __restrict__ rho_ext) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nbar) return;
   int kb = blockIdx.y * T_KCH, ke = min(K, kb + T_KCH);
@@ -428,6 +488,14 @@ __global__ void __launch_bounds__(128) k_assemble_T(
       int kp = k0 + side;                 // 0-based phi slice of the B column / B~ row
       bool lo_ok = kp - 1 >= 0, hi_ok = kp <= K - 1;
       const double* gk = gphi + (size_t)kp * NE;
+      // harmonic R_H (f4): the tables hold the arithmetic weights (R_E[sigma,i], R_f[sigma,f]);
+      // scale them to the Jacobian J_H(rho-bar^kp) / J_f at this slice
+      auto rec = [&](int ed) {
+        const double* ra = rho_ext + (size_t)(kp + 1) * nbar;
+        const double* rb = rho_ext + (size_t)kp * nbar;
+        int pL = eL[ed] / 3, pR = eR[ed] / 3;
+        return Recon::eval(1, lam[ed], 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR]));
+      };
       for (int q = 0; q < FI_MAX; q++) {
         int f = fi_cell[q * nbar + i];
         if (f < 0) break;
@@ -437,7 +505,14 @@ __global__ void __launch_bounds__(128) k_assemble_T(
         for (int e = 0; e < FI_EMAX; e++) {
           int ed = fi_edge[(q * FI_EMAX + e) * nbar + i];
           if (ed < 0) break;
-          b += fi_alpha[(q * FI_EMAX + e) * nbar + i] * gk[ed];
+          double al = fi_alpha[(q * FI_EMAX + e) * nbar + i];
+          if (harm) {
+            Recon r = rec(ed);
+            double l = lam[ed];
+            int pL = eL[ed] / 3, pR = eR[ed] / 3;
+            al *= ((pL == i ? r.ja : 0.0) + (pR == i ? r.jb : 0.0)) / ((pL == i ? l : 0.0) + (pR == i ? 1.0 - l : 0.0));
+          }
+          b += al * gk[ed];
         }
         b = b / cfv;                      // M^-1
         // row (kp, f) of B~: time part c_f (z^{hi} - z^{lo})/dt at par(f)
@@ -449,7 +524,12 @@ __global__ void __launch_bounds__(128) k_assemble_T(
         for (int t = 0; t < TB_MAX; t++) {
           int ed = fi_tbe[(q * TB_MAX + t) * nbar + i];
           if (ed < 0) break;
-          double v = b * (fi_tbbeta[(q * TB_MAX + t) * nbar + i] * gk[ed]);
+          double be = fi_tbbeta[(q * TB_MAX + t) * nbar + i];
+          if (harm) {
+            Recon r = rec(ed);
+            be *= eL[ed] == f ? r.ja / lam[ed] : r.jb / (1.0 - lam[ed]);
+          }
+          double v = b * (be * gk[ed]);
           int pL = fi_tbpL[(q * TB_MAX + t) * nbar + i], pR = fi_tbpR[(q * TB_MAX + t) * nbar + i];
           if (hi_ok) { acc[(side + 1) * W + pL] -= v; acc[(side + 1) * W + pR] += v; }
           if (lo_ok) { acc[side * W + pL] -= v; acc[side * W + pR] += v; }
@@ -603,7 +683,8 @@ void assemble_T(bbot_ctx* c) {
          (const double*)A.gphi.p, (const double*)A.omegabar.p, (const double*)A.sr.p, (const int*)g.cadj_e.p,
          (const int*)g.ca_pos.p, (const int*)g.fi_cell.p, (const int*)g.fi_child.p, (const int*)g.fi_ppos.p,
          (const int*)g.fi_edge.p, (const double*)g.fi_alpha.p, (const int*)g.fi_tbe.p, (const double*)g.fi_tbbeta.p,
-         (const int*)g.fi_tbpL.p, (const int*)g.fi_tbpR.p, A.Tv.p);
+         (const int*)g.fi_tbpL.p, (const int*)g.fi_tbpR.p, A.Tv.p, c->opts.recon, (const int*)g.eL.p,
+         (const int*)g.eR.p, (const double*)g.lam.p, (const double*)c->rho_ext.p);
 }
 
 }  // namespace bbot

@@ -57,6 +57,8 @@ void check_opts(const bbot_solver_opts& o) {
              BBOT_E_INPUT, "bad coarse sizes");
   BB_REQUIRE(o.precond >= 0 && o.precond <= 2, BBOT_E_INPUT, "precond must be 0 (BB), 1 (SIMPLE) or 2 (HSS)");
   BB_REQUIRE(o.alpha_hss > 0 && o.eps_in_hss > 0, BBOT_E_INPUT, "bad HSS alpha / eps_in");
+  BB_REQUIRE(o.recon == 0 || o.recon == 1, BBOT_E_INPUT, "recon must be 0 (arithmetic) or 1 (harmonic)");
+  BB_REQUIRE(o.recon == 0 || o.precond == 0, BBOT_E_INPUT, "the harmonic reconstruction is built for BB (precond 0)");
   BB_REQUIRE(o.coarse_max_S >= 1 && o.coarse_max_S <= 8192, BBOT_E_INPUT, "bad coarse_max_S");
 }
 
@@ -81,6 +83,7 @@ void bbot_default_solver_opts(bbot_solver_opts* o) {
   o->coarse_max_S = 256;
   o->alpha_hss = 0.5;
   o->eps_in_hss = 1e-1;
+  o->recon = 0;
 }
 
 void bbot_default_ipm_opts(bbot_ipm_opts* o) {
@@ -395,7 +398,7 @@ bbot_status bbot_ipm_run(bbot_ctx* c, const bbot_ipm_opts* po, bbot_ipm_stats* s
       bbot_ipm_record rec;
       memset(&rec, 0, sizeof(rec));
       // A34: the mu-switched BB -> SIMPLE hybrid
-      c->opts.precond = mu < o.simple_below_mu ? 1 : precond0;
+      c->opts.precond = mu < o.simple_below_mu && c->opts.recon == 0 ? 1 : precond0;
       assemble_all(c, nullptr);
       solve(c, &rec.solve);
       rec.alpha = newton_update(c, o.frac_to_boundary);

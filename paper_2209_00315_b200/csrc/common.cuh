@@ -186,6 +186,38 @@ struct DBuf {
 };
 
 // ---------------------------------------------------------------------------
+// The reconstruction of rho-bar on a fine edge: arithmetic (A3) or the weighted
+// harmonic mean (NEXT f4, A39) of the two lifted values a (left), b (right):
+//   f = 1 / (lam/a + (1-lam)/b),  df/da = lam f^2/a^2,  df/db = (1-lam) f^2/b^2,
+//   d2f/da2 = 2 lam f^2 a^-3 (lam f/a - 1),  d2f/dadb = 2 lam (1-lam) f^3 a^-2 b^-2,
+//   d2f/db2 = 2 (1-lam) f^2 b^-3 ((1-lam) f/b - 1)   (oracle/ops.py recon_*).
+struct Recon {
+  double f, ja, jb;
+  __device__ __forceinline__ static Recon eval(int harm, double lam, double a, double b) {
+    Recon r;
+    if (!harm) {
+      r.f = lam * a + (1.0 - lam) * b;
+      r.ja = lam;
+      r.jb = 1.0 - lam;
+    } else {
+      r.f = 1.0 / (lam / a + (1.0 - lam) / b);
+      double f2 = r.f * r.f;
+      r.ja = lam * f2 / (a * a);
+      r.jb = (1.0 - lam) * f2 / (b * b);
+    }
+    return r;
+  }
+  // (haa, hab, hbb) of the harmonic mean
+  __device__ __forceinline__ static void hess(double lam, double a, double b, double& haa, double& hab,
+                                              double& hbb) {
+    double f = 1.0 / (lam / a + (1.0 - lam) / b);
+    haa = 2.0 * lam * f * f / (a * a * a) * (lam * f / a - 1.0);
+    hbb = 2.0 * (1.0 - lam) * f * f / (b * b * b) * ((1.0 - lam) * f / b - 1.0);
+    hab = 2.0 * lam * (1.0 - lam) * f * f * f / (a * a * b * b);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // block reduction helpers
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -37,13 +37,16 @@ void dev_axpby(Dev& d, double alpha, const double* a, double beta, double* b, lo
 // Grid (parts, owned slices): block (p, y) handles chunk p of the y-th owned slice.  All
 // vectors are in global layout (length n); only owned slices are touched.
 
-__device__ __forceinline__ void seg_chunk(const SegArgs& A, int& s, long long& beg, long long& end) {
+// chunk [beg, end) of this block in global indices; loff: global -> slab-local basis index
+__device__ __forceinline__ void seg_chunk(const SegArgs& A, int& s, long long& beg, long long& end,
+                                          long long* loff = nullptr) {
   long long base, l;
   A.set.slice(blockIdx.y, s, base, l);
   long long chunk = (l + A.parts - 1) / A.parts;
   beg = base + (long long)blockIdx.x * chunk;
   end = base + min(l, (long long)(blockIdx.x + 1) * chunk);
   if (beg > end) beg = end;
+  if (loff) *loff = A.set.local_base(blockIdx.y) - base;
 }
 
 // out[k] = sum over slices s = 0..S-1 (in order) of tot[s][k], k < cnt; all threads of one
@@ -230,17 +233,17 @@ __global__ void k_gm_neg_norm(const double* __restrict__ a, double* __restrict__
 }
 
 // V[j] = w / s and vin = V[j], s = beta (start) or hn (Arnoldi), only if the inner loop continues
-__global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __restrict__ V,
+__global__ void k_gm_scale(long long nl, const double* __restrict__ w, double* __restrict__ V,
                            double* __restrict__ vin, const GmresScal* G, int start, SegArgs A) {
   if (!G->flag_inner) return;
   int s;
-  long long beg, end;
-  seg_chunk(A, s, beg, end);
+  long long beg, end, lo;
+  seg_chunk(A, s, beg, end, &lo);
   double sc = start ? G->beta : G->hn;
   int j = start ? 0 : G->j;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double v = w[i] / sc;
-    V[(size_t)j * n + i] = v;
+    V[(size_t)j * nl + i + lo] = v;
     vin[i] = v;
   }
 }
@@ -248,22 +251,22 @@ __global__ void k_gm_scale(long long n, const double* __restrict__ w, double* __
 // h[k] = V[k] . w for k <= j (one pass over w, one register accumulator per k);
 // optionally copy zout -> Z[j] in the same pass
 template <bool COPYZ, int NR>
-__global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __restrict__ V,
+__global__ void __launch_bounds__(256) k_gm_dots(long long nl, const double* __restrict__ V,
                                                  const double* __restrict__ w, const double* __restrict__ zout,
                                                  double* __restrict__ Z, GmresScal* G, SegArgs A) {
   const int j = G->j;
   int s;
-  long long beg, end;
-  seg_chunk(A, s, beg, end);
+  long long beg, end, lo;
+  seg_chunk(A, s, beg, end, &lo);
   double acc[NR];
 #pragma unroll
   for (int k = 0; k < NR; k++) acc[k] = 0.0;
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double wi = w[i];
-    if (COPYZ) Z[(size_t)j * n + i] = zout[i];
+    if (COPYZ) Z[(size_t)j * nl + i + lo] = zout[i];
 #pragma unroll
     for (int k = 0; k < NR; k++)
-      if (k <= j) acc[k] += V[(size_t)k * n + i] * wi;
+      if (k <= j) acc[k] += V[(size_t)k * nl + i + lo] * wi;
   }
   __shared__ double out[NR];
   if (seg_commit<NR>(acc, j + 1, A, s, out)) EpiStore{G->h1, j + 1}(out);
@@ -272,15 +275,15 @@ __global__ void __launch_bounds__(256) k_gm_dots(long long n, const double* __re
 // CGS2 middle step in one pass: w -= sum_{k<=j} h1[k] V[k] (first projection),
 // then h2[k] = V[k] . w for the second, reusing the V entries just loaded
 template <int NR>
-__global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double* __restrict__ V,
+__global__ void __launch_bounds__(256) k_gm_orth_dots(long long nl, const double* __restrict__ V,
                                                       double* __restrict__ w, GmresScal* G, SegArgs A) {
   const int j = G->j;
   __shared__ double hs[GM_MAXR + 1];
   if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = G->h1[threadIdx.x];
   __syncthreads();
   int s;
-  long long beg, end;
-  seg_chunk(A, s, beg, end);
+  long long beg, end, lo;
+  seg_chunk(A, s, beg, end, &lo);
   double acc[NR];
 #pragma unroll
   for (int k = 0; k < NR; k++) acc[k] = 0.0;
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double*
     for (int k = 0; k < NR; k++) {
       vk[k] = 0.0;
       if (k <= j) {
-        vk[k] = V[(size_t)k * n + i];
+        vk[k] = V[(size_t)k * nl + i + lo];
         sm += hs[k] * vk[k];
       }
     }
@@ -306,19 +309,19 @@ __global__ void __launch_bounds__(256) k_gm_orth_dots(long long n, const double*
 }
 
 // w -= sum_{k<=j} h2[k] V[k];  ||w|| -> Givens epilogue
-__global__ void __launch_bounds__(256) k_gm_orth(long long n, const double* __restrict__ V, double* __restrict__ w,
+__global__ void __launch_bounds__(256) k_gm_orth(long long nl, const double* __restrict__ V, double* __restrict__ w,
                                                  GmresScal* G, SegArgs A, EpiGivens epi) {
   const int j = G->j;
   __shared__ double hs[GM_MAXR + 1];
   if (threadIdx.x <= (unsigned)j) hs[threadIdx.x] = G->h2[threadIdx.x];
   __syncthreads();
   int s;
-  long long beg, end;
-  seg_chunk(A, s, beg, end);
+  long long beg, end, lo;
+  seg_chunk(A, s, beg, end, &lo);
   double acc[1] = {0.0};
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double sm = 0.0;
-    for (int k = 0; k <= j; k++) sm += hs[k] * V[(size_t)k * n + i];
+    for (int k = 0; k <= j; k++) sm += hs[k] * V[(size_t)k * nl + i + lo];
     double v = w[i] - sm;
     w[i] = v;
     acc[0] += v * v;
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(256) k_gm_orth(long long n, const double* __re
 
 // x += Z y with y = H^{-1} g (back substitution, redundantly per block); block (0,0) also
 // takes the restart decision for the outer loop
-__global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __restrict__ Z, double* __restrict__ x,
+__global__ void __launch_bounds__(256) k_gm_update(long long nl, const double* __restrict__ Z, double* __restrict__ x,
                                                    GmresScal* G, LoopCtl outer, SegArgs A) {
   __shared__ double y[GM_MAXR];
   const int jj = G->jj;
@@ -342,11 +345,11 @@ __global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __
   }
   __syncthreads();
   int s;
-  long long beg, end;
-  seg_chunk(A, s, beg, end);
+  long long beg, end, lo;
+  seg_chunk(A, s, beg, end, &lo);
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     double sm = 0.0;
-    for (int k = 0; k < jj; k++) sm += y[k] * Z[(size_t)k * n + i];
+    for (int k = 0; k < jj; k++) sm += y[k] * Z[(size_t)k * nl + i + lo];
     if (jj > 0) x[i] += sm;
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
@@ -359,10 +362,14 @@ __global__ void __launch_bounds__(256) k_gm_update(long long n, const double* __
 
 __global__ void k_gm_reset_total(GmresScal* G) { G->total_its = 0; }
 
-// parts per slice: a function of the longest slice only (P-invariant), ~2048 values per block
+// parts per slice: a function of the global slice structure only (P-invariant): ~2048 blocks
+// over all slices (enough to stream HBM; few enough that the finishing block's per-slice sums
+// -- S x parts x (j+1) partials -- stay cheap), at most one block per 1024 values
 static int seg_parts(const SliceSet& st) {
   long long L = st.S_phi > 0 ? st.N : st.nbar;
-  return (int)std::max(1LL, std::min(1024LL, (L + 2047) / 2048));
+  long long by_len = (L + 1023) / 1024;
+  long long by_grid = std::max(1LL, 2048LL / std::max(1, st.S()));
+  return (int)std::max(1LL, std::min(by_len, by_grid));
 }
 
 void DevGmres::ensure(Dev& d, const SliceSet& set_, int restart_, Comm* comm_) {
@@ -370,12 +377,13 @@ void DevGmres::ensure(Dev& d, const SliceSet& set_, int restart_, Comm* comm_) {
   set = set_;
   comm = comm_;
   parts = seg_parts(set);
-  const long long n_ = set.len();
-  if (n == n_ && restart == restart_ && V.p) return;
+  const long long n_ = set.len(), nl_ = set.len_owned();
+  if (n == n_ && nl == nl_ && restart == restart_ && V.p) return;
   n = n_;
+  nl = nl_;
   restart = restart_;
-  V.alloc((size_t)(restart + 1) * n, d.stream);
-  Z.alloc((size_t)restart * n, d.stream);
+  V.alloc((size_t)(restart + 1) * nl, d.stream);     // time slabs: the basis is slab-local (memory / P)
+  Z.alloc((size_t)restart * nl, d.stream);
   w.alloc(n, d.stream);
   vin.alloc(n, d.stream);
   zout.alloc(n, d.stream);
@@ -427,36 +435,36 @@ void DevGmres::emit(Dev& d, Reducer& red, const DevOp& op, const DevOp& pre, con
     op(x, w.p);                                               // x = 0 in the first cycle: w = 0 exactly
     launch(d, k_gm_residual, grid, dim3(BS), 0, b, w.p, seg(fused), EpiResid{G});
     finish(1, EpiResid{G});
-    launch(d, k_gm_scale, grid, dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 1, seg(fused));
+    launch(d, k_gm_scale, grid, dim3(BS), 0, nl, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 1, seg(fused));
     dev_while(d, dev_field(G, &GmresScal::flag_inner), [&](const LoopCtl& inner) {
       pre(vin.p, zout.p);
       op(zout.p, w.p);
       // CGS2: two classical Gram-Schmidt passes; the dot counts (j + 1) live on the device,
       // the finishing kernel of the split path reads them from G as well
       if (restart <= 12)
-        launch(d, k_gm_dots<true, 12>, grid, dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+        launch(d, k_gm_dots<true, 12>, grid, dim3(BS), 0, nl, (const double*)V.p, (const double*)w.p,
                (const double*)zout.p, Z.p, G, seg(fused));
       else
-        launch(d, k_gm_dots<true, GM_MAXR>, grid, dim3(BS), 0, n, (const double*)V.p, (const double*)w.p,
+        launch(d, k_gm_dots<true, GM_MAXR>, grid, dim3(BS), 0, nl, (const double*)V.p, (const double*)w.p,
                (const double*)zout.p, Z.p, G, seg(fused));
       if (!fused) {
         allgather_tot(d);
         launch(d, k_seg_finish_dots, dim3(1), dim3(BS), 0, seg(0), G, 0);
       }
       if (restart <= 12)
-        launch(d, k_gm_orth_dots<12>, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused));
+        launch(d, k_gm_orth_dots<12>, grid, dim3(BS), 0, nl, (const double*)V.p, w.p, G, seg(fused));
       else
-        launch(d, k_gm_orth_dots<GM_MAXR>, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused));
+        launch(d, k_gm_orth_dots<GM_MAXR>, grid, dim3(BS), 0, nl, (const double*)V.p, w.p, G, seg(fused));
       if (!fused) {
         allgather_tot(d);
         launch(d, k_seg_finish_dots, dim3(1), dim3(BS), 0, seg(0), G, 1);
       }
-      launch(d, k_gm_orth, grid, dim3(BS), 0, n, (const double*)V.p, w.p, G, seg(fused), EpiGivens{G, inner});
+      launch(d, k_gm_orth, grid, dim3(BS), 0, nl, (const double*)V.p, w.p, G, seg(fused), EpiGivens{G, inner});
       finish(1, EpiGivens{G, inner});
-      launch(d, k_gm_scale, grid, dim3(BS), 0, n, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0,
+      launch(d, k_gm_scale, grid, dim3(BS), 0, nl, (const double*)w.p, V.p, vin.p, (const GmresScal*)G, 0,
              seg(fused));
     });
-    launch(d, k_gm_update, grid, dim3(BS), 0, n, (const double*)Z.p, x, G, outer, seg(fused));
+    launch(d, k_gm_update, grid, dim3(BS), 0, nl, (const double*)Z.p, x, G, outer, seg(fused));
   });
 }
 

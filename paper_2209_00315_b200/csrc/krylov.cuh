@@ -45,6 +45,12 @@ struct SliceSet {
   __host__ __device__ int owned() const { return (pb - pa) + (rb - ra); }
   __host__ __device__ int S() const { return S_phi + S_rho; }
   __host__ __device__ long long len() const { return n_phi + (long long)S_rho * nbar; }
+  // values of the owned slices (the slab-local length of the Krylov basis)
+  __host__ __device__ long long len_owned() const { return (long long)(pb - pa) * N + (long long)(rb - ra) * nbar; }
+  // offset of the y-th owned slice in the slab-local basis
+  __host__ __device__ long long local_base(int y) const {
+    return y < pb - pa ? (long long)y * N : (long long)(pb - pa) * N + (long long)(y - (pb - pa)) * nbar;
+  }
   // y-th owned slice -> global slice id s, first element, length
   __device__ __forceinline__ void slice(int y, int& s, long long& base, long long& l) const {
     if (y < pb - pa) {
@@ -77,12 +83,13 @@ struct SegArgs {
 };
 
 struct DevGmres {
-  long long n = 0;
+  long long n = 0;          // global vector length (w, vin, zout, x, b: global layout)
+  long long nl = 0;         // slab-local length of the basis V, Z (= n on one rank)
   int restart = 0;
   SliceSet set;
   int parts = 1;
   Comm* comm = nullptr;
-  DBuf<double> V, Z, w, vin, zout;     // V [(r+1)][n], Z [r][n]; vin/zout: fixed pre in/out
+  DBuf<double> V, Z, w, vin, zout;     // V [(r+1)][nl], Z [r][nl] (slab-local); vin/zout: fixed pre in/out
   DBuf<double> partial, tot;
   DBuf<unsigned> counter;
   DBuf<GmresScal> sc;
@@ -150,6 +157,7 @@ __global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double*
   red_chunk(L, R.parts, beg, end);
   if (s[PS_ACTIVE * ns + k] == 0.0) end = beg;   // converged slice: frozen, nothing to do
   double acc = 0.0;
+#pragma unroll 2
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     long long row = (long long)k * L + i;
     double az = 0.0;

@@ -73,11 +73,14 @@ void remove_slice_mean(bbot_ctx* c, double* x, int ns, long long L) {
 // ---------------------------------------------------------------- B row (coarse)
 // (B x)^k_i, k = k0+1 (1-based):  Pi^T M (x^{k+1} - x^k)/dt
 //   + 1/2 sum_{sigma in E(i)} R_E[sigma,i] |e| [g^k (x^k_L - x^k_R) + g^{k+1} (x^{k+1}_L - x^{k+1}_R)]  (D5, A5)
+//   harmonic R_H (f4): R_E[sigma,i] -> J_H(rho-bar^k)[sigma,i] per slice (Lagrangian Hessian)
 struct BRow {
   int N, NE, nbar;
   double dt;
   const double *cf, *gphi, *ce_coef, *e_len;
   const int *ce_edge, *eL, *eR;
+  int harm;
+  const double *lam, *rho_ext;
   __device__ double operator()(const double* x, int k0, long long i) const {
     const double* x0 = x + (size_t)k0 * N;
     const double* x1 = x + (size_t)(k0 + 1) * N;
@@ -90,13 +93,66 @@ struct BRow {
     const double* g0 = gphi + (size_t)k0 * NE;
     const double* g1 = gphi + (size_t)(k0 + 1) * NE;
     double sp = 0.0;
+    if (!harm) {
+      for (int q = 0; q < CE_MAX; q++) {
+        int e = ce_edge[(size_t)q * nbar + i];
+        if (e < 0) break;
+        int L = eL[e], R = eR[e];
+        sp += ce_coef[(size_t)q * nbar + i] * e_len[e] * (g0[e] * (x0[L] - x0[R]) + g1[e] * (x1[L] - x1[R]));
+      }
+      return tt + 0.5 * sp;
+    }
+    const double* r0 = rho_ext + (size_t)k0 * nbar;
+    const double* r1 = rho_ext + (size_t)(k0 + 1) * nbar;
+    const double* r2 = rho_ext + (size_t)(k0 + 2) * nbar;
     for (int q = 0; q < CE_MAX; q++) {
       int e = ce_edge[(size_t)q * nbar + i];
       if (e < 0) break;
       int L = eL[e], R = eR[e];
-      sp += ce_coef[(size_t)q * nbar + i] * e_len[e] * (g0[e] * (x0[L] - x0[R]) + g1[e] * (x1[L] - x1[R]));
+      int pL = L / 3, pR = R / 3;
+      Recon a = Recon::eval(1, lam[e], 0.5 * (r1[pL] + r0[pL]), 0.5 * (r1[pR] + r0[pR]));   // phi slice k0
+      Recon b = Recon::eval(1, lam[e], 0.5 * (r2[pL] + r1[pL]), 0.5 * (r2[pR] + r1[pR]));   // phi slice k0+1
+      double ja = (pL == i ? a.ja : 0.0) + (pR == i ? a.jb : 0.0);
+      double jb = (pL == i ? b.ja : 0.0) + (pR == i ? b.jb : 0.0);
+      sp += e_len[e] * (ja * g0[e] * (x0[L] - x0[R]) + jb * g1[e] * (x1[L] - x1[R]));
     }
     return tt + 0.5 * sp;
+  }
+};
+
+// harmonic R_H (f4): (W u)_{k0,i}, W = dF_rho/drho = sum_k 1/8 (u_k u_k^T) (x) H_k (oracle ops.W):
+//   1/8 [H_{k0} (u^{k0} + u^{k0-1}) + H_{k0+1} (u^{k0} + u^{k0+1})]_i   (0-based rho slices,
+//   H_kk from phi slice kk), (H v)_i = sum_{sigma in E(i), two parents} D g^2 [h_ii v_i + h_ij v_j]
+struct WRow {
+  int nbar, NE, K;
+  const int *ce_edge, *eL, *eR;
+  const double *lam, *e_len, *w_len, *gphi, *rho_ext;
+  __device__ double operator()(const double* y, const double* shift, double sc, int k0, long long i) const {
+    auto u = [&](int k, int j) -> double {
+      if (k < 0 || k >= K) return 0.0;
+      double v = y[(size_t)k * nbar + j];
+      return shift ? v - shift[k] * sc : v;
+    };
+    double acc = 0.0;
+    for (int side = 0; side < 2; side++) {
+      int kk = k0 + side;
+      int ko = side ? k0 + 1 : k0 - 1;          // the other rho slice coupled through phi slice kk
+      const double* ra = rho_ext + (size_t)(kk + 1) * nbar;
+      const double* rb = rho_ext + (size_t)kk * nbar;
+      const double* gk = gphi + (size_t)kk * NE;
+      for (int q = 0; q < CE_MAX; q++) {
+        int e = ce_edge[(size_t)q * nbar + i];
+        if (e < 0) break;
+        int pL = eL[e] / 3, pR = eR[e] / 3;
+        if (pL == pR) continue;
+        double haa, hab, hbb;
+        Recon::hess(lam[e], 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR]), haa, hab, hbb);
+        double vL = u(k0, pL) + u(ko, pL), vR = u(k0, pR) + u(ko, pR);
+        double hv = pL == i ? haa * vL + hab * vR : hab * vL + hbb * vR;
+        acc += w_len[e] * e_len[e] * gk[e] * gk[e] * hv;
+      }
+    }
+    return 0.125 * acc;
   }
 };
 
@@ -107,6 +163,8 @@ struct BtRow {
   double dt;
   const double *cf, *gphi, *e_len, *lam;
   const int *fe, *eL, *eR;
+  int harm;
+  const double* rho_ext;
   __device__ double operator()(const double* y, const double* shift, double sc, int kk, long long f) const {
     auto u = [&](int k0, int j) -> double {
       if (k0 < 0 || k0 >= K) return 0.0;
@@ -124,7 +182,15 @@ struct BtRow {
       int L = eL[e], R = eR[e];
       int pL = L / 3, pR = R / 3;
       double l = lam[e];
-      double ru = l * (u(kk - 1, pL) + u(kk, pL)) + (1.0 - l) * (u(kk - 1, pR) + u(kk, pR));
+      double ru;
+      if (!harm) {
+        ru = l * (u(kk - 1, pL) + u(kk, pL)) + (1.0 - l) * (u(kk - 1, pR) + u(kk, pR));
+      } else {     // J_H(rho-bar^k) (f4)
+        const double* ra = rho_ext + (size_t)(kk + 1) * nbar;
+        const double* rb = rho_ext + (size_t)kk * nbar;
+        Recon r = Recon::eval(1, l, 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR]));
+        ru = r.ja * (u(kk - 1, pL) + u(kk, pL)) + r.jb * (u(kk - 1, pR) + u(kk, pR));
+      }
       double sgn = (L == f) ? 1.0 : -1.0;
       sp += sgn * e_len[e] * gk[e] * ru;
     }
@@ -134,11 +200,18 @@ struct BtRow {
 
 static BRow make_brow(bbot_ctx* c) {
   DevGeom& g = c->g;
-  return BRow{g.N, g.NE, g.nbar, g.dt, g.c.p, c->as.gphi.p, g.ce_coef.p, g.e_len.p, g.ce_edge.p, g.eL.p, g.eR.p};
+  return BRow{g.N, g.NE, g.nbar, g.dt, g.c.p, c->as.gphi.p, g.ce_coef.p, g.e_len.p, g.ce_edge.p, g.eL.p, g.eR.p,
+              c->opts.recon, g.lam.p, c->rho_ext.p};
 }
 static BtRow make_btrow(bbot_ctx* c) {
   DevGeom& g = c->g;
-  return BtRow{g.N, g.NE, g.nbar, g.K, g.dt, g.c.p, c->as.gphi.p, g.e_len.p, g.lam.p, g.fadj_e.p, g.eL.p, g.eR.p};
+  return BtRow{g.N, g.NE, g.nbar, g.K, g.dt, g.c.p, c->as.gphi.p, g.e_len.p, g.lam.p, g.fadj_e.p, g.eL.p, g.eR.p,
+               c->opts.recon, c->rho_ext.p};
+}
+static WRow make_wrow(bbot_ctx* c) {
+  DevGeom& g = c->g;
+  return WRow{g.nbar, g.NE, g.K, g.ce_edge.p, g.eL.p, g.eR.p, g.lam.p, g.e_len.p, g.w_len.p, c->as.gphi.p,
+              c->rho_ext.p};
 }
 
 // ---------------------------------------------------------------- a2: J_P
@@ -160,16 +233,19 @@ __global__ void k_jp_y1(long long n, int N, const double* __restrict__ Aoff, con
   y1[t] = acc + bt(x2, S, inv_area, kk, f);     // A x1 + B^T P^T x2
 }
 
-struct JpT {   // t = B x1 - C P^T x2, stored; returns t (for P)
+struct JpT {   // t = B x1 - C_H P^T x2 (C_H = C - W; W = 0 for R_E), stored; returns t (for P)
   BRow br;
   const double *x1, *x2, *S, *Cd;
   double inv_area;
   double* out;
   int nbar;
+  int harm;
+  WRow wr;
   __device__ double operator()(int k0, long long i) const {
     size_t t = (size_t)k0 * nbar + i;
     double u = x2[t] - S[k0] * inv_area;
     double v = br(x1, k0, i) - Cd[t] * u;
+    if (harm) v += wr(x2, S, inv_area, k0, i);
     out[t] = v;
     return v;
   }
@@ -188,12 +264,15 @@ void jp_matvec(bbot_ctx* c, const double* x, double* y) {
     c->comm->halo(c->dev, Lp, const_cast<double*>(x1));
     c->comm->halo(c->dev, Lr, const_cast<double*>(x2));
     const int pa = c->pa(), pb = c->pb(), ra = c->ra(), rb = c->rb();
-    c->red.slice_sum_range(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, std::max(0, ra - 1), rb, K, S1);
+    // c-bar sums of the left halo slice (B^T P^T) -- and of the right one for W (harmonic)
+    c->red.slice_sum_range(WSlice{g.cbar.p, x2, g.nbar}, g.nbar, std::max(0, ra - 1),
+                           c->opts.recon ? std::min(K, rb + 1) : rb, K, S1);
     launch(c->dev, k_jp_y1, dim3(nblocks((long long)(pb - pa) * g.N, BS)), dim3(BS), 0, (long long)pb * g.N, g.N,
            (const double*)c->as.Aoff.p, (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
            1.0 / g.area, y, (long long)pa * g.N);
-    c->red.slice_sum_range(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, ra, rb, K,
-                           S2);
+    c->red.slice_sum_range(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar, c->opts.recon,
+                               make_wrow(c)},
+                           g.nbar, ra, rb, K, S2);
     if (rb > ra)
       launch(c->dev, k_sub_slice_w_rng, dim3(nblocks((long long)(rb - ra) * g.nbar, BS)), dim3(BS), 0,
              (long long)g.nbar, (long long)ra * g.nbar, (long long)rb * g.nbar, y + n, (const double*)g.cbar.p,
@@ -204,7 +283,9 @@ void jp_matvec(bbot_ctx* c, const double* x, double* y) {
   launch(c->dev, k_jp_y1, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)c->as.Aoff.p,
          (const int*)g.fadj_nb.p, make_btrow(c), x1, x2, (const double*)S1,
          1.0 / g.area, y, 0LL);
-  c->red.slice_sum(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar}, g.nbar, K, S2, false);
+  c->red.slice_sum(JpT{make_brow(c), x1, x2, S1, c->as.Cd.p, 1.0 / g.area, y + n, g.nbar, c->opts.recon,
+                       make_wrow(c)},
+                   g.nbar, K, S2, false);
   launch(c->dev, k_sub_slice_w, dim3(nblocks(m, BS)), dim3(BS), 0, (long long)g.nbar, K, y + n,
          (const double*)g.cbar.p, (const double*)S2, 1.0 / g.area);
 }
@@ -433,6 +514,14 @@ __global__ void k_user_shift(long long n, long long m, int N, BtRow bt, const do
     h[t - n] -= s[t - n] * drho0[t - n];                                // h - s drho0
   }
 }
+// harmonic R_H (f4): g -= W drho0 (the (2,2) block acts on the slice-mass part too)
+__global__ void k_user_gshift(long long m, int nbar, WRow wr, const double* __restrict__ drho0,
+                              const double* __restrict__ gin, double* __restrict__ gout) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k0 = (int)(t / nbar);
+  gout[t] = gin[t] - wr(drho0, nullptr, 0.0, k0, t - (long long)k0 * nbar);
+}
 __global__ void k_add(long long n, const double* __restrict__ a, double* __restrict__ b) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) b[t] += a[t];
@@ -461,6 +550,11 @@ void set_user_rhs(bbot_ctx* c) {   // as.f, as.g, as.h hold the caller's (f; g; 
          c->drho0.p);
   launch(c->dev, k_user_shift, dim3(nblocks(n + m, BS)), dim3(BS), 0, n, m, g.N, make_btrow(c),
          (const double*)c->drho0.p, (const double*)c->s.p, A.f.p, A.h.p);
+  if (c->opts.recon) {
+    BB_CUDA(cudaMemcpyAsync(A.gt.p, A.g.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    launch(c->dev, k_user_gshift, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, make_wrow(c),
+           (const double*)c->drho0.p, (const double*)A.gt.p, A.g.p);
+  }
   // g~ and the right-hand side of (4.17) / the saddle-point system
   launch(c->dev, k_user_gt, dim3(nblocks(m, BS)), dim3(BS), 0, m, g.nbar, (const double*)g.cbar.p,
          (const double*)A.g.p, (const double*)A.h.p, (const double*)(c->rho_ext.p + g.nbar), A.gt.p);
@@ -485,13 +579,17 @@ void finish_user_solve(bbot_ctx* c) {   // drho += drho0
 }
 
 // ---------------------------------------------------------------- a6 recovery
-struct QSum {  // q = g~ - B dphit + C drho ; returns q
+struct QSum {  // q = g~ - B dphit + C_H drho ; returns q  (C_H = C - W, W = 0 for R_E)
   BRow br;
   const double *dphit, *drho, *gt, *Cd;
   int nbar;
+  int harm;
+  WRow wr;
   __device__ double operator()(int k0, long long i) const {
     size_t t = (size_t)k0 * nbar + i;
-    return gt[t] - br(dphit, k0, i) + Cd[t] * drho[t];
+    double q = gt[t] - br(dphit, k0, i) + Cd[t] * drho[t];
+    if (harm) q -= wr(drho, nullptr, 0.0, k0, i);
+    return q;
   }
 };
 
@@ -539,7 +637,8 @@ static void recover_slab(bbot_ctx* c) {
   c->red.slice_sum_range(WSlice{g.c.p, dphit, g.N}, g.N, pa, pb, K + 1, S);
   sub_slice(c, dphit, g.N, pa, pb, K + 1, S, 1.0 / g.area);
   c->comm->halo(c->dev, Layout::uniform(K + 1, g.N), dphit);
-  c->red.slice_sum_range(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar}, g.nbar, ra, rb, K, S);
+  if (c->opts.recon) c->comm->halo(c->dev, Layout::uniform(K, g.nbar), c->drho.p);   // W couples k-1, k+1
+  c->red.slice_sum_range(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar, c->opts.recon, make_wrow(c)}, g.nbar, ra, rb, K, S);
   c->comm->allgather(c->dev, Layout::uniform(K, 1), S);
   launch(c->dev, k_prefix_shift, dim3(1), dim3(32), 0, K, g.dt, 1.0 / g.area, (const double*)S, shift);
   launch(c->dev, k_add_shift, dim3(nblocks((long long)(pb - pa) * g.N, BS)), dim3(BS), 0, (long long)pb * g.N, g.N,
@@ -583,7 +682,7 @@ void recover(bbot_ctx* c) {
   launch(c->dev, k_sub_slice, dim3(nblocks(n, BS)), dim3(BS), 0, (long long)g.N, K + 1, dphit, (const double*)S,
          1.0 / g.area);
   // dlambda = E-bar(g~ - B dphit + C drho)/|Omega|
-  c->red.slice_sum(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar}, g.nbar, K, S, false);
+  c->red.slice_sum(QSum{make_brow(c), dphit, c->drho.p, c->as.gt.p, c->as.Cd.p, g.nbar, c->opts.recon, make_wrow(c)}, g.nbar, K, S, false);
   launch(c->dev, k_prefix_shift, dim3(1), dim3(32), 0, K, g.dt, 1.0 / g.area, (const double*)S, shift);
   launch(c->dev, k_add_shift, dim3(nblocks(n, BS)), dim3(BS), 0, n, g.N, (const double*)dphit, (const double*)shift,
          c->dphi.p, 0LL);
@@ -647,13 +746,14 @@ struct KeF {
   int N, NE, nbar;
   const int *eL, *eR;
   const double *lam, *e_len, *w_len, *phi, *rho_ext;
+  int harm;
   __device__ double operator()(int kk, long long e) const {
     int L = eL[e], R = eR[e];
     int pL = L / 3, pR = R / 3;
     const double* ra = rho_ext + (size_t)(kk + 1) * nbar;
     const double* rb = rho_ext + (size_t)kk * nbar;
     double l = lam[e];
-    double rt = l * (0.5 * (ra[pL] + rb[pL])) + (1.0 - l) * (0.5 * (ra[pR] + rb[pR]));
+    double rt = Recon::eval(harm, l, 0.5 * (ra[pL] + rb[pL]), 0.5 * (ra[pR] + rb[pR])).f;   // R_E or R_H
     double dphi = phi[(size_t)kk * N + L] - phi[(size_t)kk * N + R];
     return e_len[e] * rt / w_len[e] * dphi * dphi;       // phi^T A_k phi edge by edge
   }
@@ -662,7 +762,7 @@ struct KeF {
 double kinetic_energy(bbot_ctx* c) {
   DevGeom& g = c->g;
   double* S = c->scal.p;
-  c->red.slice_sum(KeF{g.N, g.NE, g.nbar, g.eL.p, g.eR.p, g.lam.p, g.e_len.p, g.w_len.p, c->phi.p, c->rho_ext.p},
+  c->red.slice_sum(KeF{g.N, g.NE, g.nbar, g.eL.p, g.eR.p, g.lam.p, g.e_len.p, g.w_len.p, c->phi.p, c->rho_ext.p, c->opts.recon},
                    g.NE, g.K + 1, S, false);
   std::vector<double> h(g.K + 1);
   BB_CUDA(cudaMemcpyAsync(h.data(), S, (g.K + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->dev.stream));

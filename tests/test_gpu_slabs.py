@@ -27,11 +27,11 @@ def _gpu():
     return pb
 
 
-def _ranks(pb, p, P):
+def _ranks(pb, p, P, opts=None):
     import torch
     grp = next(_group)
     streams = [torch.cuda.Stream() for _ in range(P)]
-    ctxs = [pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=st.cuda_stream) for st in streams]
+    ctxs = [pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, stream=st.cuda_stream, opts=opts) for st in streams]
     for r, c in enumerate(ctxs):
         c.set_dist_virtual(r, P, grp)
     return ctxs, streams
@@ -128,6 +128,29 @@ def test_slab_newton_solve_bitwise(name, kind, mu, P):
             assert np.array_equal(u, v)
     K1 = p.K + 1
     assert slabs == [(r * K1 // P, (r + 1) * K1 // P) for r in range(P)]
+
+
+def test_slab_newton_solve_bitwise_harmonic():
+    """The decomposed solve with the harmonic reconstruction (NEXT f4: the W block couples
+    neighbouring density slices in J_P and the recovery -- two-sided halos): bitwise equal to
+    one GPU on P = 3 virtual ranks."""
+    pb = _gpu()
+    p, phi, rho, s = _state("C1", "random", 1e-2)
+    opts = pb.default_solver_opts(recon=1)
+    ref = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f, opts=opts)
+    ref.set_state(phi, rho, s, 1e-2)
+    ref.assemble()
+    dphi, drho, ds, st = ref.solve()
+    ctxs, _ = _ranks(pb, p, 3, opts=pb.default_solver_opts(recon=1))
+
+    def work(rank, c):
+        c.set_state(phi, rho, s, 1e-2)
+        c.assemble()
+        return c.solve()
+    for rank, (gphi, grho, gds, gst) in enumerate(_parallel(ctxs, work)):
+        for u, v in ((gphi, dphi), (grho, drho), (gds, ds)):
+            assert np.array_equal(u, v), (rank, np.abs(u - v).max())
+        assert gst["outer_its"] == st["outer_its"]
 
 
 def test_slab_rejects_too_many_ranks():

@@ -141,3 +141,30 @@ def test_harmonic_ipm_kinetic_energy_translation():
     gap = [kes[(L, "harm")] - kes[(L, "arith")] for L in (1, 2)]
     assert 0 < eh[1] < 0.8 * eh[0], kes                  # converging from above
     assert 0 < gap[1] < 0.6 * gap[0], kes                # R_H >= ... -> R_E: the gap closes
+
+
+def test_harmonic_solve_rhs_matches_direct():
+    """solve(rhs) with R_H: the slice-mass step now also carries W δρ₀ into g (the (2,2) block
+    acts on it); the result is the dense least-squares solve of (3.1) with the caller's (f;g;h),
+    on a state of the harmonic IPM trajectory (mu = 2^-4)."""
+    from oracle.ipm import IpmOpts, ipm_run
+    from synthetic import initial_state
+    p, d = _disc("T1")
+    phi, rho, s = initial_state(p, 1.0)
+    r = ipm_run(d, phi, rho, s, IpmOpts(mu_min=2.0 ** -4), SolverOpts())
+    phi, rho, s = r.phi, r.rho, r.s
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal(d.n)
+    f -= f.mean()
+    g, h = rng.standard_normal(d.m), rng.standard_normal(d.m)
+    S = BBSolver(d, phi, rho, s, 2.0 ** -5, SolverOpts(eps_out=1e-12))
+    dphi, drho, ds = S.solve_rhs(f, g, h)
+    assert S.stats["converged"], S.stats
+    J = d.jacobian(phi, rho, s).toarray()
+    rhs = np.concatenate([f, g, h])
+    ref, *_ = np.linalg.lstsq(J, rhs, rcond=None)
+    n, m = d.n, d.m
+    rp = ref[:n].reshape(d.K + 1, d.N)
+    rp = (rp - (rp[0] @ d.M) / d.area).reshape(-1)
+    for a, b in ((dphi, rp), (drho, ref[n:n + m]), (ds, ref[n + m:])):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b)
