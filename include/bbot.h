@@ -76,6 +76,12 @@ typedef struct {
    * shifted Laplacians A^_k + a I (eq:solve-laplacians); both inner solves to eps_in_hss. */
   double alpha_hss;    /* HSS relaxation parameter [0.5]                              */
   double eps_in_hss;   /* HSS inner tolerance [1e-1]                                  */
+  int recon;           /* density reconstruction on the fine edges [0]: 0 = weighted
+                        * arithmetic mean (A3); 1 = weighted HARMONIC mean (NEXT f4, Remark 3.3,
+                        * DESIGN.md A39-A41): A_k, F_phi, F_rho, B, B^T, the kinetic energy and
+                        * the Newton (2,2) block W = dF_rho/drho follow R_H; (4.17) carries
+                        * C_H = C - W, the BB preconditioner diag(C_H) in T, the coarse harmonic
+                        * mean in Atilde and the fine Jacobian in Btilde.  BB only.          */
 } bbot_solver_opts;
 
 typedef struct {

@@ -402,8 +402,6 @@ __global__ void k_up_dot(V v, const double* __restrict__ dinv, const double* __r
   red_chunk(L, R.parts, beg, end);
   if (active && active[k] == 0.0) end = beg;     // converged slice: nothing to do (partial 0)
   double dot = 0.0;
-  // two rows in flight per thread: the neighbour -> agg -> xc gathers of independent rows overlap
-#pragma unroll 2
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     long long r = (long long)k * L + i;
     double acc = b[r];

@@ -63,12 +63,14 @@ __device__ __forceinline__ void seg_total(const SegArgs& A, int cnt, double* out
   __syncthreads();
 }
 
-// block partials of cnt values; the last block turns the owned slices' partials into slice
-// totals and (fused) the slice totals into out[0..cnt).  Returns true in every thread of the
-// block that must run the epilogue.
+// block partials of cnt values; the last block of each slice turns that slice's partials into
+// its slice totals (fixed order over the parts), and the last slice to finish (fused) the
+// slice totals into out[0..cnt).  Returns true in every thread of the block that must run
+// the epilogue.
 template <int NR>
 __device__ __forceinline__ bool seg_commit(const double (&acc)[NR], int cnt, const SegArgs& A, int s, double* out) {
   __shared__ double shn[NR][33];
+  __shared__ int s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int k = 0; k < NR; k++)
@@ -85,21 +87,33 @@ __device__ __forceinline__ bool seg_commit(const double (&acc)[NR], int cnt, con
       __threadfence();
     }
   }
-  if (!red_last_block(A.counter)) return false;
-  const int ny = A.set.owned();
-  for (int q = w; q < ny * cnt; q += nw) {
-    int y = q / cnt, k = q - y * cnt;
-    int ss;
-    long long b0, l0;
-    A.set.slice(y, ss, b0, l0);
+  __syncthreads();
+  if (threadIdx.x == 0) {       // last block of this slice?
+    __threadfence();
+    unsigned t = atomicAdd(A.counter + 1 + s, 1u);
+    s_last = (t == (unsigned)A.parts - 1) ? 1 : 0;
+    if (s_last) A.counter[1 + s] = 0u;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  for (int k = w; k < cnt; k += nw) {
     double v = 0.0;
-    for (int p = lane; p < A.parts; p += 32) v += __ldcg(A.partial + ((size_t)ss * A.parts + p) * GM_NRP + k);
+    for (int p = lane; p < A.parts; p += 32) v += __ldcg(A.partial + ((size_t)s * A.parts + p) * GM_NRP + k);
     v = warp_sum(v);
-    if (lane == 0) A.tot[(size_t)ss * GM_NRP + k] = v;
+    if (lane == 0) A.tot[(size_t)s * GM_NRP + k] = v;
   }
   __threadfence();
   __syncthreads();
-  if (!A.fused) return false;
+  if (threadIdx.x == 0) {       // last slice of the launch?
+    unsigned t = atomicAdd(A.counter, 1u);
+    s_last = (t == (unsigned)A.set.owned() - 1) ? 1 : 0;
+    if (s_last) {
+      __threadfence();
+      A.counter[0] = 0u;
+    }
+  }
+  __syncthreads();
+  if (!s_last || !A.fused) return false;
   seg_total(A, cnt, out);
   return true;
 }
@@ -362,13 +376,12 @@ __global__ void __launch_bounds__(256) k_gm_update(long long nl, const double* _
 
 __global__ void k_gm_reset_total(GmresScal* G) { G->total_its = 0; }
 
-// parts per slice: a function of the global slice structure only (P-invariant): ~2048 blocks
-// over all slices (enough to stream HBM; few enough that the finishing block's per-slice sums
-// -- S x parts x (j+1) partials -- stay cheap), at most one block per 1024 values
+// parts per slice: a function of the global slice structure only (P-invariant): ~4096 blocks
+// over all slices (several waves to stream HBM), at most one block per 1024 values
 static int seg_parts(const SliceSet& st) {
   long long L = st.S_phi > 0 ? st.N : st.nbar;
   long long by_len = (L + 1023) / 1024;
-  long long by_grid = std::max(1LL, 2048LL / std::max(1, st.S()));
+  long long by_grid = std::max(1LL, 4096LL / std::max(1, st.S()));
   return (int)std::max(1LL, std::min(by_len, by_grid));
 }
 
@@ -390,8 +403,8 @@ void DevGmres::ensure(Dev& d, const SliceSet& set_, int restart_, Comm* comm_) {
   partial.alloc((size_t)set.S() * parts * GM_NRP, d.stream);
   tot.alloc((size_t)set.S() * GM_NRP, d.stream);
   tot.zero();
-  if (!counter.p) {
-    counter.alloc(1, d.stream);
+  if (counter.n != (size_t)set.S() + 1) {
+    counter.alloc((size_t)set.S() + 1, d.stream);
     counter.zero();
   }
   if (!sc.p) {

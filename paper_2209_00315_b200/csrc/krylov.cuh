@@ -78,7 +78,7 @@ struct SegArgs {
   int parts;
   double* partial;      // [S][parts][GM_NRP]
   double* tot;          // [S][GM_NRP]
-  unsigned* counter;
+  unsigned* counter;    // [1 + S]: slices finished; per slice: blocks finished
   int fused;            // 1: the last block finishes (single rank)
 };
 
@@ -157,7 +157,6 @@ __global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double*
   red_chunk(L, R.parts, beg, end);
   if (s[PS_ACTIVE * ns + k] == 0.0) end = beg;   // converged slice: frozen, nothing to do
   double acc = 0.0;
-#pragma unroll 2
   for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
     long long row = (long long)k * L + i;
     double az = 0.0;
