@@ -266,3 +266,20 @@ def test_solve_rhs_newton_rhs_is_plain_solve():
     b = S2.solve_rhs(S2.f, S2.g, S2.h)
     for u, v in zip(a, b):
         assert np.allclose(u, v, rtol=0, atol=1e-13 * max(1.0, abs(v).max()))
+
+
+def test_direct_newton_is_the_least_squares_min_norm_solution():
+    """oracle/direct.py (the pin of every Krylov direction): its bordered sparse solve
+    [[J, v], [vᵀ, 0]] with the kernel v = (1;0;0) of Remark 3.1 equals the dense
+    least-squares minimum-norm solution of (3.1) (then the A11 gauge)."""
+    for name in ("T0", "T1"):
+        p = make_problem(name)
+        d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+        phi, rho, s = random_state(p, seed=7, mu=0.05)
+        dphi, drho, ds, J, rhs = direct_newton(d, phi, rho, s, 0.05)
+        ref, *_ = np.linalg.lstsq(J.toarray(), rhs, rcond=None)
+        n, m = d.n, d.m
+        rp = ref[:n].reshape(d.K + 1, d.N)
+        rp = (rp - (rp[0] @ d.M) / d.area).reshape(-1)
+        for a, b in ((dphi, rp), (drho, ref[n:n + m]), (ds, ref[n + m:])):
+            assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
