@@ -16,3 +16,13 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def root():
     return ROOT
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _single_thread_blas():
+    """The oracle's library primitives run single-threaded in the tests: deterministic
+    summation order (the per-system parity tests compare against it) and no BLAS thread
+    oversubscription on the small dense/sparse products of the CPU suite."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        yield
