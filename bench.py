@@ -138,9 +138,12 @@ class ByteModel:
     pattern [W][nbar] int32 once); coarse AMG levels as SELL-32 (12 B per stored entry).
     Multigrid kernels run on every level with a different grid: a launch is mapped to its
     level by its CTA count (nblocks(rows, 256)).  Krylov kernels: CGS2 over j+1 basis
-    vectors, j = the mean Arnoldi index of this solve's own iteration counts."""
+    vectors, j = the mean Arnoldi index of this solve's own iteration counts.
+    The per-slice PCG and every AMG(A) kernel skip the rows of converged time slices, so
+    their bytes per launch are the full-launch bytes times the mean fraction of active
+    slices, act = (slice-iterations of the solve) / (PCG launches x (K+1))."""
 
-    def __init__(self, ctx, st, opts=None):
+    def __init__(self, ctx, st, opts=None, pcg_launches=None):
         self.n, self.m, self.N, self.K, self.nbar = ctx.n, ctx.m, ctx.N, ctx.K, ctx.nbar
         self.NE = ctx.NE
         nnzT, W = ctx.T_nnz()
@@ -154,6 +157,20 @@ class ByteModel:
         self.its_T = st["inner_T_its"]
         self.jO = _arnoldi_mean_j(self.its_O, r_out)
         self.jT = _arnoldi_mean_j(max(1, round(self.its_T / self.its_O)), r_T)
+        self.act = 1.0
+        if pcg_launches:
+            self.act = min(1.0, st["inner_A_its_total"] / (pcg_launches * (self.K + 1)))
+
+    def bytes(self, name, grid):
+        b = self._bytes(name, grid)
+        if b is None:
+            return None
+        base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
+        a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView>" in base
+        if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict"):
+            lv = self._level(grid, by="nc" if base == "k_restrict" else "n")
+            a_side = lv is not None and lv[0] == "A"
+        return b * self.act if a_side else b
 
     def _level(self, grid, by="n"):
         """(hierarchy, level, (n, nnz, nc)) whose row (or coarse-row) count gives `grid` CTAs."""
@@ -172,7 +189,7 @@ class ByteModel:
             b += 12 * max(nnz, 0) + 40 * n + 8 * nc
         return b
 
-    def bytes(self, name, grid):
+    def _bytes(self, name, grid):
         n, m, N, K, NE = self.n, self.m, self.N, self.K, self.NE
         nm = n + m
         base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
@@ -244,10 +261,11 @@ def roofline_of(ctx, st, prof_grid, opts=None):
     """Roofline of the TOP kernel by device time, from one eagerly issued step's per-launch
     CUDA-event table (kernel, grid) -> (launches, ms): achieved = algorithmic bytes of its
     launches / their measured time."""
-    bm = ByteModel(ctx, st, opts)
+    pcg = sum(c for (nm, _g), (c, _ms) in prof_grid.items() if "k_pcg_pq" in nm)
+    bm = ByteModel(ctx, st, opts, pcg_launches=pcg)
     per = {}
     for (name, grid), (cnt, ms) in prof_grid.items():
-        e = per.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0.0, "modeled": True})
+        e = per.setdefault(name, {"launches": 0, "ms": 0.0, "bytes": 0.0, "full": 0.0, "modeled": True})
         e["launches"] += cnt
         e["ms"] += ms
         b = bm.bytes(name, grid)
@@ -255,6 +273,7 @@ def roofline_of(ctx, st, prof_grid, opts=None):
             e["modeled"] = False
         else:
             e["bytes"] += b * cnt
+            e["full"] += bm._bytes(name, grid) * cnt
     total_ms = sum(e["ms"] for e in per.values())
     ranked = sorted(per.items(), key=lambda kv: -kv[1]["ms"])
     peak, peak_kind = hbm_peak()
@@ -265,11 +284,14 @@ def roofline_of(ctx, st, prof_grid, opts=None):
                      "share": round(e["ms"] / total_ms, 4),
                      "GBps": round(ach, 1) if ach is not None else None,
                      "frac": round(ach / peak, 4) if ach is not None else None,
-                     "bytes_per_launch": (e["bytes"] / e["launches"]) if e["modeled"] else None})
+                     "bytes_per_launch": (e["bytes"] / e["launches"]) if e["modeled"] else None,
+                     "full_launch_bytes": (e["full"] / e["launches"]) if e["modeled"] else None})
     top = rows[0]
     roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": top["GBps"], "peak": peak, "unit": "GB/s",
             "frac": top["frac"], "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
             "algorithmic_bytes_per_launch": top["bytes_per_launch"],
+            "algorithmic_bytes_full_launch": top["full_launch_bytes"],
+            "active_slice_fraction": round(bm.act, 4),
             "avg_launch_us": round(1e3 * top["ms"] / top["launches"], 2), "launches_per_step": top["launches"],
             "share_of_step": top["share"]}
     # bytes-weighted achieved bandwidth of every modeled kernel (the step's HBM efficiency)
@@ -591,10 +613,12 @@ def main():
         launches = ctx.launch_count() - l0
         roof, kernels, total_ms = roofline_of(ctx, last["st"], prof)
         traffic, rnd = ncu_traffic(args.config, roof["kernel"])
-        if traffic is not None and roof["algorithmic_bytes_per_launch"]:
+        if traffic is not None and roof["algorithmic_bytes_full_launch"]:
+            # ncu captures a launch with every time slice active: compare with the full-launch model
             roof["traffic"] = traffic
-            roof["traffic_source"] = f"profiles/ncu_summary.json ({args.config}, ncu --set full, {rnd} code)"
-            roof["traffic_over_algorithmic"] = round(traffic / roof["algorithmic_bytes_per_launch"], 3)
+            roof["traffic_source"] = (f"profiles/ncu_summary.json ({args.config}, ncu --set full, {rnd} code, "
+                                      f"a launch with every slice active)")
+            roof["traffic_over_algorithmic"] = round(traffic / roof["algorithmic_bytes_full_launch"], 3)
         if args.profile_out and rank == 0:
             json.dump({"config": args.config, "kernels": kernels, "total_ms": total_ms},
                       open(args.profile_out, "w"), indent=1)

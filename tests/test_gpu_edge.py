@@ -138,3 +138,27 @@ def test_C3_direction_satisfies_newton_system():
         assert o["converged"] and abs(st["outer_its"] - o["outer_its"]) <= 1, (st, o)
 
 
+
+
+def test_C4_first_system_counts_match_oracle():
+    """The bench headline system (BASELINE configs[3], C4: 131 072 cells, K = 128, 67.5 M
+    unknowns): the GPU's first IPM Newton solve converges with the oracle's own outer count
+    +-1 (tests/golden/oracle_counts.json: scripts/oracle_counts.py, oracle only, ~2 h and
+    ~30 GB on one core) and the same inner T-GMRES count within the +-1 outer slack."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_counts.json")))
+    o = gold.get("C4/init/mu=1")
+    if o is None:
+        pytest.skip("C4 oracle counts not generated")
+    pb = _gpu()
+    p = make_problem("C4")
+    phi, rho, s = initial_state(p, 1.0)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    ctx.assemble()
+    st = ctx.solve_stats_only()
+    print("C4 gpu", {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "rel_res")}, "oracle", o)
+    assert o["converged"] and st["converged"] == 1
+    assert abs(st["outer_its"] - o["outer_its"]) <= 1, (st, o)
+    assert abs(st["inner_T_its"] - o["inner_T_its"]) <= 50, (st, o)
