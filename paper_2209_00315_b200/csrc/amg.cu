@@ -560,7 +560,12 @@ struct TailPos {               // this CTA: slice k, rank c of cs CTAs in the sl
   __device__ long long stride() const { return (long long)cs * blockDim.x; }
 };
 
-__device__ __forceinline__ void tail_sync() { cg::this_cluster().sync(); }
+// a one-CTA cluster (the default) synchronises with a block barrier: bar.sync instead of the
+// cluster-scope release/acquire barrier, ~a hundred of which separate the levels of one tail
+__device__ __forceinline__ void tail_sync(const TailPos& P) {
+  if (P.cs == 1) __syncthreads();
+  else cg::this_cluster().sync();
+}
 
 // per-slice dot over rows [s0, s1): block sums, then every CTA adds the cluster's
 // partials in rank order (identical result everywhere)
@@ -571,6 +576,13 @@ __device__ __forceinline__ double tail_dot(const double* u, const double* v, lon
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) acc += u[r] * v[r];
   acc = block_sum(acc);
   if (threadIdx.x == 0) part = acc;
+  if (P.cs == 1) {                 // the same sum as the loop below with one term
+    __syncthreads();
+    double tot = 0.0;
+    tot += part;
+    __syncthreads();
+    return tot;
+  }
   cg::cluster_group cl = cg::this_cluster();
   cl.sync();
   double tot = 0.0;
@@ -587,7 +599,7 @@ __device__ void tail_kstep(const TailArgs* __restrict__ T, int q, const TailPos&
   const TailLevel& L = T->lv[q];
   const long long s0 = L.sptr[P.k], s1 = L.sptr[P.k + 1];
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.krc[r] = L.b[r];
-  tail_sync();
+  tail_sync(P);
   tail_cycle(T, q, P);                                   // c1 -> xo
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
     L.kc1[r] = L.xo[r];
@@ -595,12 +607,12 @@ __device__ void tail_kstep(const TailArgs* __restrict__ T, int q, const TailPos&
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
     L.kv[r] = av;                                        // v1 = A c1
   }
-  tail_sync();
+  tail_sync(P);
   const double rho1 = tail_dot(L.kc1, L.kv, s0, s1, P);
   const double a1 = tail_dot(L.kc1, L.krc, s0, s1, P);
   const double f1 = tail_div(a1, rho1);
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.b[r] = L.krc[r] - f1 * L.kv[r];   // r2
-  tail_sync();
+  tail_sync(P);
   tail_cycle(T, q, P);                                   // c2 -> xo
   const double g = tail_dot(L.xo, L.kv, s0, s1, P);
   const double a2 = tail_dot(L.xo, L.b, s0, s1, P);
@@ -609,13 +621,13 @@ __device__ void tail_kstep(const TailArgs* __restrict__ T, int q, const TailPos&
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
     L.kv[r] = av;                                        // v2 = A c2
   }
-  tail_sync();
+  tail_sync(P);
   const double beta = tail_dot(L.xo, L.kv, s0, s1, P);
   const double rho2 = beta - g * tail_div(g, rho1);
   const double g2 = tail_div(a2, rho2);
   const double e1 = f1 - g * tail_div(g2, rho1);
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.xo[r] = e1 * L.kc1[r] + g2 * L.xo[r];
-  tail_sync();
+  tail_sync(P);
 }
 
 // cycle of tail level q: input lv[q].b, output lv[q].xo
@@ -637,7 +649,7 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
           for (int l = 0; l < nloc; l++) acc += inv[j * T->cm + l] * C.b[s0 + l];
           C.xo[s0 + j] = acc;
         }
-      tail_sync();
+      tail_sync(P);
       return;
     }
     for (int j = tid; j < nloc; j += bs) {      // every CTA of the cluster computes it (tiny)
@@ -656,7 +668,7 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
     __syncthreads();
     if (P.c == 0)
       for (int j = tid; j < nloc; j += bs) C.xo[s0 + j] = xs[j] - mean;
-    tail_sync();
+    tail_sync(P);
     return;
   }
   const TailLevel& L = T->lv[q];
@@ -667,7 +679,7 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
     L.x[r] = om * L.dinv[r] * L.b[r];
     L.r[r] = acc;
   }
-  tail_sync();
+  tail_sync(P);
   const TailLevel& C = T->lv[q + 1];
   const long long c0 = C.sptr[P.k], c1 = C.sptr[P.k + 1];
   for (long long I = P.first_row(c0); I < c1; I += P.stride()) {
@@ -675,7 +687,7 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
     for (long long p = L.mptr[I]; p < L.mptr[I + 1]; p++) acc += L.r[L.midx[p]];
     C.b[I] = acc;
   }
-  tail_sync();
+  tail_sync(P);
   if (C.kc) tail_kstep(T, q + 1, P);
   else tail_cycle(T, q + 1, P);
   const double* xc = C.xo;
@@ -684,7 +696,7 @@ __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos&
     L.A.row(r, [&](long long c, double a) { acc -= a * (L.x[c] + xc[L.agg[c]]); });
     L.xo[r] = (L.x[r] + xc[L.agg[r]]) + om * L.dinv[r] * acc;
   }
-  tail_sync();
+  tail_sync(P);
 }
 
 __global__ void __launch_bounds__(TAIL_BS) k_tailA(const TailArgs* __restrict__ T, const double* active) {
@@ -700,7 +712,7 @@ __global__ void __launch_bounds__(TAIL_BS) k_tailA(const TailArgs* __restrict__ 
       F.b[I] = acc;
     }
   }
-  tail_sync();
+  tail_sync(P);
   if (T->lv[0].kc) tail_kstep(T, 0, P);
   else tail_cycle(T, 0, P);
 }
