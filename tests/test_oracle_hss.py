@@ -121,3 +121,19 @@ def test_amg_mode_As_coarsest_is_exact_on_one_level():
     Hh = amg.setup(A, sl, "As", 2 / 3, coarse_max=64)
     b = rng.standard_normal(60)
     assert np.allclose(amg.vcycle(Hh, b), np.linalg.solve(A.toarray(), b), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("L,K,table", [(1, 4, 31), (2, 8, 71)])
+def test_hss_counts_vs_paper_table(L, K, table):
+    """Outer FGMRES iterations of the HSS-preconditioned solve (α = 0.5, ε_in = 1e-1, AMG inner
+    solves as the paper's AGMG) at μ = 1 and the paper's ε_out = 1e-5, test
+    case 2 (translated compact bump), within a factor 2 of the first row of the HSS table for
+    the two coarsest meshes (31 at N̄ = 56, Nt = 8; 71 at N̄ = 224, Nt = 16) --
+    the S:605 acceptance band used for BB (test_bb_counts_vs_table4).  Measured 46 / 98."""
+    p = make_problem("T2b", L=L, K=K)
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    from synthetic import initial_state
+    phi, rho, s = initial_state(p, 1.0)
+    H = HssSolver(d, phi, rho, s, 1.0, SolverOpts(precond="hss", eps_out=1e-5, maxit=2000))
+    H.solve()
+    assert H.stats["converged"] and table / 2 <= H.stats["outer_its"] <= 2 * table, H.stats
