@@ -394,7 +394,7 @@ __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restr
 // level-0 prolongation + post-smoothing fused with the per-slice dot b.xo
 // (grid (parts, ns) over slice-major rows; PCG: r.z with its beta epilogue)
 template <class V>
-__global__ void k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+__global__ void __launch_bounds__(256, 8) k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
                          const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
                          double* __restrict__ xo, long long L, RedArgs R, PcgRzFin fin, const double* active) {
   int k = blockIdx.y;

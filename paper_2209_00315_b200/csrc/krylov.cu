@@ -527,7 +527,7 @@ __global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double
   if (red_commit(acc, R)) fin(R.out);
 }
 
-__global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+__global__ void __launch_bounds__(256, 8) k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                          const double* __restrict__ q, double* s, const int* its, PcgScal* P, double tol, RedArgs R,
                          LoopCtl ctl) {
   int k = blockIdx.y;

@@ -142,13 +142,13 @@ __global__ void k_pcg_start(long long L, const double* __restrict__ b, double* _
 __global__ void k_pcg_rz(long long L, const double* __restrict__ r, const double* __restrict__ z, RedArgs R,
                          PcgRzFin fin);
 // x += alpha p, r -= alpha q; rn; active &= rn > tol bn; it++; loop condition; stats at exit
-__global__ void k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+__global__ void __launch_bounds__(256, 8) k_pcg_xr(long long L, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                          const double* __restrict__ q, double* s, const int* its, PcgScal* P, double tol, RedArgs R,
                          LoopCtl L_);
 
 // p = z + beta p;  q = A z + beta q  (= A p, since q held A p_old);  partial p.q
 template <class V>
-__global__ void k_pcg_pq(V v, long long L, const double* __restrict__ z, double* __restrict__ p,
+__global__ void __launch_bounds__(256, 8) k_pcg_pq(V v, long long L, const double* __restrict__ z, double* __restrict__ p,
                          double* __restrict__ q, const double* __restrict__ s, RedArgs R, PcgAlphaFin fin) {
   int k = blockIdx.y;
   int ns = gridDim.y;
