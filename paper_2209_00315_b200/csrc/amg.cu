@@ -524,6 +524,7 @@ static const long long TAIL_ROWS = tune_env("BBOT_TAIL_ROWS", 0);       // A-tai
 static const long long TAILT_ROWS = tune_env("BBOT_TAILT_ROWS", 16384); // first T-tail level: <= rows in total
 static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tail cluster size (0: 148/slices)
 static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
+static const int TAILA_THREADS = (int)tune_env("BBOT_TAILA_BS", 1024);   // k_tailA block size (<= TAIL_BS)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
 constexpr int TAIL_MAXL = 24;
@@ -1409,7 +1410,8 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
   if (H.mode != 1 && H.tail > 0) {
     int cl = TAIL_CL > 0 ? std::min(TAIL_CL, TAIL_MAXCL)
                          : std::max(1, std::min(TAIL_MAXCL, d.num_sms / std::max(1, H.nslices)));
-    launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(TAIL_BS), 0, cl, (const TailArgs*)H.tail_args.p, active);
+    launch_cluster(d, k_tailA, dim3(H.nslices * cl), dim3(std::min(TAIL_BS, TAILA_THREADS)), 0, cl,
+                   (const TailArgs*)H.tail_args.p, active);
   } else if (H.tail > 0) {
     launch_cluster(d, k_tailT, dim3(H.tail_cl), dim3(TAIL_BS), 0, H.tail_cl, (const TailTArgs*)H.tail_args.p, 1);
   } else {

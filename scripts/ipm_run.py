@@ -39,8 +39,9 @@ def main():
     st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=a.mu_min, simple_below_mu=a.simple_below),
                             callback=cb)
     wall = time.time() - t
-    print(json.dumps({"config": a.config, "n_systems": st["n_systems"], "total_outer": st["total_outer"],
-                      "n_unconverged": st["n_unconverged"], "n_simple_fallback": st["n_simple_fallback"],
+    print(json.dumps({"config": a.config, "mu_min": a.mu_min, "n_systems": st["n_systems"],
+                      "n_converged": st["n_systems"] - st["n_unconverged"], "total_outer": st["total_outer"],
+                      "n_unconverged": st["n_unconverged"],
                       "final_mu": st["final_mu"],
                       "kinetic_energy": st["kinetic_energy"], "wall_s": round(wall, 2),
                       "solves_per_s": st["n_systems"] / wall}))
