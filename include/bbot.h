@@ -271,8 +271,15 @@ bbot_status bbot_get_slab(const bbot_ctx* ctx, int* k_begin, int* k_end);
 /* The ownership rule of the exchange layer (host only, no GPU): rank `rank` of `nranks` owns
  * the slices [*lo, *hi) of a slice-structured vector with S slices when the slabs are cut
  * over Kp1 = K+1 potential slices; its halos are slices *lo-1 (from rank-1) and *hi (from
- * rank+1).  For the exchange-plan tests. */
+ * rank+1).  Slabs are unions of whole AMG(T) time blocks (bbot_time_blocks): the first
+ * slice of rank r is B * floor(r * nb / P) (the last rank also owns slice K).  For the
+ * exchange-plan tests.  BBOT_E_INPUT on a bad rank / count. */
 bbot_status bbot_slab_plan(int Kp1, int nranks, int rank, int S, int* lo, int* hi);
+/* The time blocks of AMG(T) (A42; the aggregation unit of T, whose rows couple
+ * consecutive time slices through the time Laplacian in -B M^-1 B~, eq. (4.26)):
+ * *block_size = B = max(1, floor(K/8)) consecutive density slices, *nblocks = floor(K/B),
+ * the last block taking the remainder.  Host only.  BBOT_E_INPUT if K < 1. */
+bbot_status bbot_time_blocks(int K, int* block_size, int* nblocks);
 
 /* Execution mode of bbot_solve.  1 (default): the whole solve -- FGMRES, the BB
  * applies with their inner GMRES / per-slice PCG loops, recovery -- is captured

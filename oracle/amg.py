@@ -7,8 +7,9 @@ same definition, and only this oracle pins it (plus the generic AMG sanity
 pins in tests: Galerkin identity, symmetry of the V-cycle, convergence).
 
 Definition (both sides):
-  * rows are grouped in slices (time levels); couplings across slices are never
-    used for aggregation (block-diagonal A_k: none exist; T: within-slice only).
+  * rows are grouped in slices (time levels) -- for AMG(T) in time BLOCKS of consecutive
+    slices (time_blocks below, A42); couplings across slices (blocks) are never
+    used for aggregation (block-diagonal A_k: none exist; T: within a time block only).
   * strength s_ij = (|a_ij| + |a_ji|)/2, j != i, same slice (symmetrised so that
     mutual-maximum matching always progresses on nonsymmetric T).
   * pairwise matching, 16 synchronous rounds: every free row i with
@@ -50,6 +51,21 @@ KC_MIN_LEVELS = 7   # ... in hierarchies of >= KC_MIN_LEVELS levels.  Plain aggr
 #                    C2 (5 levels) but 64 on C4 (8 levels); the K-cycle on the coarse levels
 #                    brings C4 back to ~31, while on the shallow C2 it only costs
 _M32 = np.uint64(0xFFFFFFFF)
+
+
+def time_blocks(K: int) -> np.ndarray:
+    """A42: the aggregation unit of AMG(T).  T couples consecutive time slices (the time
+    Laplacian -B M^-1 B~ ⊇ D_t M̄ D_t^T, A8); aggregating within single slices never coarsens
+    that coupling, and after a few spatial levels it dominates (it grows with the aggregate
+    mass while the 2D spatial Galerkin couplings do not): T-GMRES needed 15 iterations per
+    outer iteration at K = 128 against the paper's 1.7-5.7.  So T's rows are grouped
+    in B = max(1, floor(K/8)) consecutive density slices -- 8 blocks, the last one taking the
+    remainder -- and aggregates may span the slices of a block.  8 blocks keep the
+    decomposition into P <= 8 time slabs exact (slab boundaries on block boundaries, §8(e)).
+    Returns the block of each slice (K,)."""
+    B = max(1, K // 8)
+    nb = max(1, K // B)
+    return np.minimum(np.arange(K) // B, nb - 1)
 
 
 def prio(j):

@@ -69,7 +69,7 @@ class BBSolver:
             self.Apinv = [np.linalg.pinv(Ak.toarray()) for Ak in d.A_blocks(rho)]
         else:
             slA = np.repeat(np.arange(d.K + 1), d.N)
-            slT = np.repeat(np.arange(d.K), d.nbar)
+            slT = np.repeat(amg.time_blocks(d.K), d.nbar)          # A42: time blocks
             self.amgA = amg.setup(self.A, slA, "A", o.omega_A, o.coarse_max_A)
             self.amgT = amg.setup(self.T, slT, "T", o.omega_T, o.coarse_max_T)
 

@@ -8,8 +8,8 @@ there is deliberately no CPU fallback.
 """
 from ._bbot import (BBOT_MEM_DEVICE, BBOT_MEM_HOST, EXPORTED, LIB_PATH, BbotError, Context, IpmOpts,
                     SolveStats, SolverOpts, default_ipm_opts, default_solver_opts, lib, nccl_unique_id,
-                    slab_plan)
+                    slab_plan, time_blocks)
 
 __all__ = ["Context", "SolverOpts", "IpmOpts", "SolveStats", "BbotError", "default_solver_opts",
            "default_ipm_opts", "lib", "LIB_PATH", "EXPORTED", "BBOT_MEM_HOST", "BBOT_MEM_DEVICE", "nccl_unique_id",
-           "slab_plan"]
+           "slab_plan", "time_blocks"]

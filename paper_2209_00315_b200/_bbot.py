@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbbot.so")
+LIB_PATH = os.environ.get("BBOT_LIB") or os.path.join(_HERE, "libbbot.so")   # BBOT_LIB: A/B builds
 
 BBOT_MEM_HOST, BBOT_MEM_DEVICE = 0, 1
 STATUS = {0: "OK", 1: "E_INPUT", 2: "E_GEOMETRY", 3: "E_STATE", 4: "E_NOCONV", 5: "E_CUDA",
@@ -106,6 +106,7 @@ _sigs = {
     "bbot_set_dist_virtual": (C.c_int, [_P, C.c_int, C.c_int, C.c_longlong]),
     "bbot_get_slab": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bbot_slab_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "bbot_time_blocks": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bbot_prof_start": (C.c_int, [_P]),
     "bbot_prof_stop": (C.c_int, [_P, C.c_char_p, C.c_longlong, C.POINTER(C.c_longlong)]),
 }
@@ -138,6 +139,15 @@ def slab_plan(Kp1: int, nranks: int, rank: int, S: int):
     if st != 0:
         raise BbotError(st, "bbot_slab_plan: bad arguments")
     return lo.value, hi.value
+
+
+def time_blocks(K: int):
+    """(B, nb): the AMG(T) time blocks of a K-slice problem (bbot_time_blocks, A42)."""
+    b, nb = C.c_int(), C.c_int()
+    st = lib.bbot_time_blocks(int(K), C.byref(b), C.byref(nb))
+    if st != 0:
+        raise BbotError(st, "bbot_time_blocks: bad arguments")
+    return b.value, nb.value
 
 
 def default_solver_opts(**kw) -> SolverOpts:

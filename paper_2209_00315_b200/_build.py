@@ -29,17 +29,19 @@ def _newest_header():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, build_dir: str = BUILD,
+          extra=()) -> str:
+    """extra: additional nvcc flags (A/B variants: own build_dir and lib, e.g. -DBBOT_LAP_MINB=6)."""
+    os.makedirs(build_dir, exist_ok=True)
     hdr = _newest_header()
     objs, jobs = [], []
     for s in sources():
         src = os.path.join(CSRC, s)
-        obj = os.path.join(BUILD, s + ".o")
+        obj = os.path.join(build_dir, s + ".o")
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr):
             lang = [] if s.endswith(".cu") else ["-x", "cu"]
-            jobs.append([NVCC, *ARCH, *FLAGS, *lang, "-c", src, "-o", obj])
+            jobs.append([NVCC, *ARCH, *FLAGS, *extra, *lang, "-c", src, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,9 +53,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if jobs or not os.path.exists(LIB):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])  # NCCL: dlopen
-    return LIB
+    if jobs or not os.path.exists(lib):
+        run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])  # NCCL: dlopen
+    return lib
 
 
 if __name__ == "__main__":

@@ -394,7 +394,7 @@ __global__ void k_up(V v, const double* __restrict__ dinv, const double* __restr
 // level-0 prolongation + post-smoothing fused with the per-slice dot b.xo
 // (grid (parts, ns) over slice-major rows; PCG: r.z with its beta epilogue)
 template <class V>
-__global__ void __launch_bounds__(256, 8) k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+__global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_up_dot(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
                          const double* __restrict__ x, const int* __restrict__ agg, const double* __restrict__ xc,
                          double* __restrict__ xo, long long L, RedArgs R, PcgRzFin fin, const double* active) {
   int k = blockIdx.y;
@@ -1451,12 +1451,23 @@ void amg_vcycle_slab(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, dou
   BB_REQUIRE(H.mode == 1, BBOT_E_INTERNAL, "amg_vcycle_slab: mode-T hierarchies only");
   const int L = (int)H.lv.size();
   const double om = H.omega;
+  // level 0 is slice-structured (T couples slice k with k +- 1: one-slice halos); the coarse
+  // levels are grouped by time block (A42: aggregates span the slices of a block), so their
+  // halos are whole neighbouring blocks and the rank's rows are its blocks [ra/B, rb/B)
+  const int K = v0.K;
+  const long long tnbar = v0.nbar;
+  const int TB = time_block_size(K);
   auto lay = [&](int l) {
+    if (l == 0) return Layout::uniform(K, tnbar);
     Layout Ly;
     Ly.off = H.lv[l].sptr;
+    Ly.unit = TB;
     return Ly;
   };
-  auto rng = [&](int l) { return RowRange{H.lv[l].sptr[ra], H.lv[l].sptr[rb]}; };
+  auto rng = [&](int l) {
+    if (l == 0) return RowRange{(long long)ra * tnbar, (long long)rb * tnbar};
+    return RowRange{H.lv[l].sptr[ra / TB], H.lv[l].sptr[std::min(rb / TB, H.nslices)]};
+  };
   auto grid = [&](const RowRange& r) { return dim3(nblocks(std::max(1LL, r.r1 - r.r0), BS)); };
   const SliceSkip none{nullptr, nullptr, 1};
   if (L == 1) {                        // level 0 is the coarsest: solve it redundantly

@@ -191,10 +191,11 @@ void upload_geometry(bbot_ctx* c, const Geometry& hg, int K) {
   g.fi_tbpL.upload(fi_tbpL, s);
   g.fi_tbpR.upload(fi_tbpR, s);
   g.ca_pos.upload(ca_pos, s);
-  // AMG level-0 slice maps
+  // AMG level-0 slice maps (AMG(T): row -> time block)
   std::vector<int> slA((size_t)N * (K + 1)), slT((size_t)nbar * K);
   for (int k = 0; k <= K; k++) std::fill(slA.begin() + (size_t)k * N, slA.begin() + (size_t)(k + 1) * N, k);
-  for (int k = 0; k < K; k++) std::fill(slT.begin() + (size_t)k * nbar, slT.begin() + (size_t)(k + 1) * nbar, k);
+  for (int k = 0; k < K; k++)   // AMG(T): time blocks (A42)
+    std::fill(slT.begin() + (size_t)k * nbar, slT.begin() + (size_t)(k + 1) * nbar, time_block_of(K, k));
   g.slice_A.upload(slA, s);
   g.slice_T.upload(slT, s);
   std::vector<int> slS((size_t)nbar * K, 0);

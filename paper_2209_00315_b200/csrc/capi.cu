@@ -554,6 +554,13 @@ bbot_status bbot_slab_plan(int Kp1, int nranks, int rank, int S, int* lo, int* h
   return BBOT_OK;
 }
 
+bbot_status bbot_time_blocks(int K, int* block_size, int* nblocks) {
+  if (K < 1 || !block_size || !nblocks) return BBOT_E_INPUT;
+  *block_size = time_block_size(K);
+  *nblocks = time_blocks(K);
+  return BBOT_OK;
+}
+
 bbot_status bbot_get_slab(const bbot_ctx* c, int* k_begin, int* k_end) {
   if (!c) return BBOT_E_INPUT;
   if (k_begin) *k_begin = c->nranks > 1 ? c->own_begin : 0;

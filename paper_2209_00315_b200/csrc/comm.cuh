@@ -2,9 +2,11 @@
 //
 // Every slice-structured vector lives in GLOBAL layout on every rank (slice k at the same
 // offset everywhere); a rank computes only the slices of its slab.  Rank q of P owns the
-// potential slices [a_q, a_{q+1}), a_q = floor(q (K+1) / P), and -- for every vector whose
-// slices are density (time-level) slices, S = K of them, and for every level of AMG(T),
-// whose coarse rows stay slice-grouped -- the slices [min(a_q, S), min(a_{q+1}, S)).
+// potential slices [a_q, a_{q+1}), a_q = B floor(q nb / P) (whole time blocks of B slices,
+// A42; a_P = K+1), and -- for every vector whose slices are density (time-level) slices,
+// S = K of them -- the slices [min(a_q, S), min(a_{q+1}, S)); on the coarse levels of
+// AMG(T), whose rows are grouped by time block (Layout::unit = B), the blocks
+// [a_q / B, min(a_{q+1} / B, nb)).
 // A Layout is the slice offsets of one such vector (S + 1 entries, host).
 //
 // Two operations, both in place on the global-layout buffer:
@@ -25,6 +27,7 @@ namespace bbot {
 
 struct Layout {
   std::vector<long long> off;     // S + 1 element offsets
+  int unit = 1;                   // density slices per layout entry (AMG(T) coarse levels: a time block)
   int S() const { return (int)off.size() - 1; }
   static Layout uniform(int S, long long len, long long base = 0) {
     Layout L;
@@ -34,19 +37,29 @@ struct Layout {
   }
 };
 
-int slab_begin(int nslices, int rank, int nranks);
-// owned slices [lo, hi) of rank q for a layout of S slices (slab basis: Kp1 potential slices)
-inline void slab_owned(int Kp1, int nranks, int q, int S, int& lo, int& hi) {
-  lo = std::min(slab_begin(Kp1, q, nranks), S);
-  hi = std::min(slab_begin(Kp1, q + 1, nranks), S);
+// A42: AMG(T) aggregates within time blocks of B = max(1, floor(K/8)) consecutive density
+// slices (nb = floor(K/B) blocks, the last one taking the remainder) -- the same rule as
+// oracle/amg.py::time_blocks.  The slabs are unions of whole blocks, so the decomposition
+// stays exact (P <= nb).
+inline int time_block_size(int K) { return std::max(1, K / 8); }
+inline int time_blocks(int K) { return std::max(1, K / time_block_size(K)); }
+inline int time_block_of(int K, int k) { return std::min(k / time_block_size(K), time_blocks(K) - 1); }
+
+// first potential slice of rank `rank` (rank == nranks: Kp1): a_r = B floor(r nb / P)
+int slab_begin(int Kp1, int rank, int nranks);
+// owned entries [lo, hi) of rank q for a layout of S entries of `unit` slices each
+// (slab basis: Kp1 potential slices; unit > 1 only on block-aligned slab boundaries)
+inline void slab_owned(int Kp1, int nranks, int q, int S, int& lo, int& hi, int unit = 1) {
+  lo = std::min(slab_begin(Kp1, q, nranks) / unit, S);
+  hi = std::min(slab_begin(Kp1, q + 1, nranks) / unit, S);
 }
 
 class Comm {
  public:
   int rank = 0, nranks = 1, Kp1 = 1;      // Kp1: number of potential slices (slab basis)
   virtual ~Comm() {}
-  // owned slices [lo, hi) of a layout with S slices
-  void owned(int S, int q, int& lo, int& hi) const { slab_owned(Kp1, nranks, q, S, lo, hi); }
+  // owned entries [lo, hi) of a layout
+  void owned(const Layout& L, int q, int& lo, int& hi) const { slab_owned(Kp1, nranks, q, L.S(), lo, hi, L.unit); }
   virtual void halo(Dev& d, const Layout& L, double* base) = 0;
   virtual void allgather(Dev& d, const Layout& L, double* base) = 0;
   virtual void barrier(Dev& d) = 0;

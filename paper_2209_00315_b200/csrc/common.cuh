@@ -15,6 +15,12 @@
 #include <algorithm>
 #include "../../include/bbot.h"
 
+// resident CTAs per SM requested by the fused level-0 A_k kernels (k_pcg_pq, k_up_dot):
+// 8 x 256 threads caps them at 32 registers (full occupancy; the gathers are latency-bound)
+#ifndef BBOT_LAP_MINB
+#define BBOT_LAP_MINB 8
+#endif
+
 namespace bbot {
 
 struct Error : public std::runtime_error {

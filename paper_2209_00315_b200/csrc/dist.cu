@@ -14,8 +14,10 @@
 
 namespace bbot {
 
-int slab_begin(int nslices, int rank, int nranks) {
-  return (int)(((long long)rank * nslices) / nranks);
+int slab_begin(int Kp1, int rank, int nranks) {
+  if (rank >= nranks) return Kp1;
+  const int K = Kp1 - 1;
+  return time_block_size(K) * (int)(((long long)rank * time_blocks(K)) / nranks);
 }
 
 // ------------------------------------------------------------------ NCCL backend
@@ -71,7 +73,7 @@ class NcclComm : public Comm {
     NcclApi& a = nccl();
     const int S = L.S();
     int lo, hi;
-    owned(S, rank, lo, hi);
+    owned(L, rank, lo, hi);
     check(a.GroupStart(), "ncclGroupStart");
     if (rank > 0 && lo > 0 && hi > lo) {
       check(a.Send(base + L.off[lo], (size_t)(L.off[lo + 1] - L.off[lo]), ncclDouble, rank - 1, comm, d.stream),
@@ -80,7 +82,7 @@ class NcclComm : public Comm {
             "ncclRecv");
     }
     int nlo, nhi;
-    owned(S, rank + 1, nlo, nhi);
+    owned(L, rank + 1, nlo, nhi);
     if (rank + 1 < nranks && hi < S && nhi > nlo) {
       check(a.Send(base + L.off[hi - 1], (size_t)(L.off[hi] - L.off[hi - 1]), ncclDouble, rank + 1, comm, d.stream),
             "ncclSend");
@@ -95,7 +97,7 @@ class NcclComm : public Comm {
     check(a.GroupStart(), "ncclGroupStart");
     for (int q = 0; q < nranks; q++) {
       int lo, hi;
-      owned(L.S(), q, lo, hi);
+      owned(L, q, lo, hi);
       if (hi <= lo) continue;
       double* p = base + L.off[lo];
       check(a.Broadcast(p, p, (size_t)(L.off[hi] - L.off[lo]), ncclDouble, q, comm, d.stream), "ncclBroadcast");
@@ -162,10 +164,10 @@ class VirtComm : public Comm {
     post(d, base);
     const int S = L.S();
     int lo, hi;
-    owned(S, rank, lo, hi);
+    owned(L, rank, lo, hi);
     if (rank > 0 && lo > 0 && hi > lo) copy(d, base + L.off[lo - 1], grp->ptr[rank - 1] + L.off[lo - 1], L.off[lo] - L.off[lo - 1]);
     int nlo, nhi;
-    owned(S, rank + 1, nlo, nhi);
+    owned(L, rank + 1, nlo, nhi);
     if (rank + 1 < nranks && hi < S && nhi > nlo)
       copy(d, base + L.off[hi], grp->ptr[rank + 1] + L.off[hi], L.off[hi + 1] - L.off[hi]);
     done(d);
@@ -176,7 +178,7 @@ class VirtComm : public Comm {
     for (int q = 0; q < nranks; q++) {
       if (q == rank) continue;
       int lo, hi;
-      owned(L.S(), q, lo, hi);
+      owned(L, q, lo, hi);
       if (hi > lo) copy(d, base + L.off[lo], grp->ptr[q] + L.off[lo], L.off[hi] - L.off[lo]);
     }
     done(d);
@@ -228,8 +230,8 @@ void nccl_unique_id(unsigned char out[128]) {
 // uid != NULL: NCCL (one process per GPU); uid == NULL: virtual ranks of group `group`
 void set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid, long long group) {
   BB_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, BBOT_E_INPUT, "bad rank / nranks");
-  BB_REQUIRE(nranks == 1 || 2 * nranks <= c->g.K + 1, BBOT_E_INPUT,
-             "time slabs: every rank needs >= 2 potential slices (2 P <= K + 1)");
+  BB_REQUIRE(nranks == 1 || nranks <= time_blocks(c->g.K), BBOT_E_INPUT,
+             "time slabs: every rank needs >= 1 time block (P <= max(1, K / max(1, K/8)))");
   drop_dist(c);
   drop_solve_graph(c);
   c->rank = rank;

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, 8) k_pcg_xr(long long L, double* __restri
 
 // p = z + beta p;  q = A z + beta q  (= A p, since q held A p_old);  partial p.q
 template <class V>
-__global__ void __launch_bounds__(256, 8) k_pcg_pq(V v, long long L, const double* __restrict__ z, double* __restrict__ p,
+__global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_pcg_pq(V v, long long L, const double* __restrict__ z, double* __restrict__ p,
                          double* __restrict__ q, const double* __restrict__ s, RedArgs R, PcgAlphaFin fin) {
   int k = blockIdx.y;
   int ns = gridDim.y;

@@ -62,7 +62,7 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
     amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_S.p, 1, 1, o.omega_T, o.coarse_max_S, w);
   } else if (c->dev.prof || !c->dev2.stream) {   // sequential (the per-launch profiler records one stream)
     amg_setup(c->dev, c->amgA, view_A(c), c->g.slice_A.p, c->g.K + 1, 0, o.omega_A, o.coarse_max_A, w);
-    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, w);
+    amg_setup(c->dev, c->amgT, view_T(c), c->g.slice_T.p, time_blocks(c->g.K), 1, o.omega_T, o.coarse_max_T, w);
   } else {
     // The two setups are independent and host-latency-bound (size read-backs between
     // kernels): AMG(T) runs on a second stream from a second host thread, after the
@@ -83,7 +83,7 @@ void assemble_all(bbot_ctx* c, bbot_solve_stats* st) {
       try {
         BB_CUDA(cudaSetDevice(devid));   // a new host thread starts on device 0
         auto a = now();
-        amg_setup(c->dev2, c->amgT, view_T(c), c->g.slice_T.p, c->g.K, 1, o.omega_T, o.coarse_max_T, c->amgw2);
+        amg_setup(c->dev2, c->amgT, view_T(c), c->g.slice_T.p, time_blocks(c->g.K), 1, o.omega_T, o.coarse_max_T, c->amgw2);
         sync(c->dev2);
         tT = std::chrono::duration<double, std::milli>(now() - a).count();
       } catch (...) {

@@ -2,7 +2,8 @@
 inner counts on the first IPM Newton system (A19 point, mu = 1) of the configs (calls only
 oracle/ and synthetic/, one core).  The GPU parity tests hold the CUDA path to these counts
 (+-1 outer) on the configs too large to re-run the oracle inside a test (C2: ~1 min, C3:
-~15 min on one core)."""
+~15 min, C4: hours on one core).  ORACLE_COUNTS_OUT=<file>: write there instead (parallel
+runs, merged afterwards)."""
 import json
 import os
 import sys
@@ -16,7 +17,7 @@ from oracle.bb import BBSolver, SolverOpts  # noqa: E402
 from oracle.ops import Discretisation  # noqa: E402
 from synthetic import initial_state, make_problem  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
+OUT = os.environ.get("ORACLE_COUNTS_OUT") or os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
 
 
 def main(names):

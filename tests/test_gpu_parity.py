@@ -44,7 +44,8 @@ def _setup(name, state="random", mu=1e-2, seed=3, **kw):
     return pb, p, d, ctx, (phi, rho, s, mu)
 
 
-CASES = [("T1", {}), ("C1", {}), ("T2b", {})]
+# ("T2", K=32): AMG(T) time blocks of B = 4 slices (A42; K <= 15 gives single-slice blocks)
+CASES = [("T1", {}), ("C1", {}), ("T2b", {}), ("T2", {"K": 32})]
 
 
 @pytest.mark.parametrize("name,kw", CASES)

@@ -93,7 +93,8 @@ def test_slab_jp_and_bb_apply_bitwise(P):
 
 
 @pytest.mark.parametrize("name,kind,mu,P", [("C1", "init", 1.0, 3), ("C1", "random", 1e-2, 2),
-                                            ("T2", "random", 5e-2, 4), ("C2", "init", 1.0, 4)])
+                                            ("T2", "random", 5e-2, 4), ("C2", "init", 1.0, 4),
+                                            ("C2", "init", 1.0, 3), ("T0", "init", 1.0, 2)])
 def test_slab_newton_solve_bitwise(name, kind, mu, P):
     """The whole Newton solve (FGMRES on (4.17) with the BB preconditioner, recovery a6) on P
     virtual ranks: the direction on every rank equals the single-GPU direction bitwise, with the
@@ -126,8 +127,9 @@ def test_slab_newton_solve_bitwise(name, kind, mu, P):
         assert a == a1
         for u, v in zip(state[:3], s1[:3]):
             assert np.array_equal(u, v)
-    K1 = p.K + 1
-    assert slabs == [(r * K1 // P, (r + 1) * K1 // P) for r in range(P)]
+    B, nb = pb.time_blocks(p.K)        # slabs: whole AMG(T) time blocks (A42)
+    starts = [B * (r * nb // P) for r in range(P)] + [p.K + 1]
+    assert slabs == [(starts[r], starts[r + 1]) for r in range(P)]
 
 
 def test_slab_newton_solve_bitwise_harmonic():
@@ -154,9 +156,10 @@ def test_slab_newton_solve_bitwise_harmonic():
 
 
 def test_slab_rejects_too_many_ranks():
-    """2P <= K+1 (every rank needs >= 2 potential slices): T0 (K = 2) cannot take P = 2."""
+    """P <= nb (every rank owns >= 1 AMG(T) time block, A42): T0 (K = 2, two single-slice
+    blocks) cannot take P = 3."""
     pb = _gpu()
     p = make_problem("T0")
     c = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     with pytest.raises(pb.BbotError):
-        c.set_dist_virtual(0, 2, 99)
+        c.set_dist_virtual(0, 3, 99)

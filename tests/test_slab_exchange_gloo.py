@@ -5,8 +5,9 @@ needed), then runs the halo exchange with the NCCL backend's pairing (send the f
 slice left / receive slice lo-1; send the last owned slice right / receive slice hi) and the
 allgather as one broadcast per owner -- on layouts with unequal slice lengths (the AMG(T)
 coarse levels) and S = K or K+1 slices.  Checks: the slices are owned exactly once, every
-rank owns >= 1 slice when 2P <= K+1, the halos hold the neighbours' values, the allgather
-reproduces the global vector on every rank."""
+rank owns >= 1 slice when P <= nb (the AMG(T) time blocks, A42), slab boundaries fall on
+block boundaries, the halos hold the neighbours' values, the allgather reproduces the global
+vector on every rank."""
 import os
 import socket
 import sys
@@ -85,8 +86,10 @@ def _exchange(rank, world, K, dist, torch, pb, res):
             res.append((S, plan, ok_halo, bool(np.array_equal(buf.numpy(), glob))))
 
 
-@pytest.mark.parametrize("world,K", [(2, 4), (3, 8), (3, 5)])
+@pytest.mark.parametrize("world,K", [(2, 4), (3, 8), (3, 5), (3, 32)])
 def test_slab_exchange_gloo(world, K):
+    sys.path.insert(0, ROOT)
+    import paper_2209_00315_b200 as pb
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -103,5 +106,26 @@ def test_slab_exchange_gloo(world, K):
         for S, plan, ok_halo, ok_all in res:
             owned = [s for a, b in plan for s in range(a, b)]
             assert owned == list(range(S))                 # every slice exactly once, in order
-            assert all(b > a for a, b in plan)             # 2P <= K+1: nobody idle
+            assert all(b > a for a, b in plan)             # P <= nb: nobody idle
+            B, nb = pb.time_blocks(K)
+            assert all(a % B == 0 for a, _ in plan)        # slabs are unions of time blocks
             assert ok_halo and ok_all, (rank, S)
+
+
+@pytest.mark.parametrize("K", [1, 2, 4, 5, 8, 12, 32, 64, 128, 256])
+def test_time_blocks_rule_matches_oracle(K):
+    """A42: the GPU library's time blocks (bbot_time_blocks) and the oracle's
+    (oracle/amg.py::time_blocks) are the same partition of the K density slices, and for
+    P = 1..min(8, nb) every slab boundary of bbot_slab_plan is a block boundary."""
+    sys.path.insert(0, ROOT)
+    import paper_2209_00315_b200 as pb
+    from oracle.amg import time_blocks
+    B, nb = pb.time_blocks(K)
+    blk = time_blocks(K)
+    assert blk.max() + 1 == nb and np.array_equal(blk, np.minimum(np.arange(K) // B, nb - 1))
+    for P in range(1, min(8, nb) + 1):
+        plan = [pb.slab_plan(K + 1, P, r, K) for r in range(P)]
+        assert [s for a, b in plan for s in range(a, b)] == list(range(K))
+        assert all(b > a for a, b in plan)
+        starts = {0} | {int(k) for k in np.nonzero(np.diff(blk))[0] + 1}
+        assert all(a in starts for a, _ in plan)
