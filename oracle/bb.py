@@ -6,6 +6,7 @@ Ideal block-triangular preconditioner (4.18)-(4.20), with the Schur
 complement replaced through the approximate commutation (4.22), and
 solved as (4.26).  BB apply on (r1; r2):
   (i)   T z = -r2  by GMRES(10) + one AMG(T) V-cycle, relative eps_T (1e-1)
+        (A43: the target is max(eps_T ||r2||, 1e-12 ||r||), rounding-level r2 is not solved)
   (ii)  y = P^T (M̄^{-1} Ã z)
   (iii) b = r1 - B^T P^T y;  b^k -= mean(b^k)            (compatibility)
   (iv)  A_k x^k = b^k by PCG + AMG(A_k) V-cycle, relative eps_A (A14: 1e-3), x^k -= mean
@@ -22,6 +23,9 @@ import numpy as np
 from . import amg
 from .krylov import fgmres, pcg_slices
 from .ops import Discretisation
+
+
+T_NOISE = 1e-12      # A43: delta of the T-solve's stopping rule (relative to ||(r1; r2)||)
 
 
 @dataclass
@@ -81,9 +85,12 @@ class BBSolver:
         if o.exact_inner:
             z = self.Tinv @ (-r2)
         else:
+            # A43: stop at max(eps_T ||r2||, delta ||r||) -- an r2 at rounding level of r
+            # (P g~ at the A19 point is zero in exact arithmetic) is not solved to eps_T relative
             nr2 = float(np.linalg.norm(r2))
+            scale = max(nr2, T_NOISE / o.eps_T * float(np.linalg.norm(r)))
             z, itT, _, _ = fgmres(lambda v: self.T @ v, lambda v: amg.vcycle(self.amgT, v),
-                                  -r2, nr2, o.eps_T, o.restart_T, o.maxit_inner)
+                                  -r2, scale, o.eps_T, o.restart_T, o.maxit_inner)
             self.inner_T_its += itT
         y = d.PT((self.Atilde @ z) / self.Mbar_t)
         b = (r1 - self.BT @ d.PT(y)).reshape(d.K + 1, d.N)

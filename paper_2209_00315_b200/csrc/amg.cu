@@ -524,6 +524,7 @@ static const long long TAIL_ROWS = tune_env("BBOT_TAIL_ROWS", 0);       // A-tai
 static const long long TAILT_ROWS = tune_env("BBOT_TAILT_ROWS", 16384); // first T-tail level: <= rows in total
 static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tail cluster size (0: 148/slices)
 static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
+static const bool SELL_SPLIT = tune_env("BBOT_SELL_SPLIT", 0) != 0;    // T coarse levels: prolong + post
 static const int TAILA_THREADS = (int)tune_env("BBOT_TAILA_BS", 1024);   // k_tailA block size (<= TAIL_BS)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
@@ -1438,6 +1439,11 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
              (const int*)lv.agg.p, xc, out, skip_at(0));
+    } else if (H.mode == 1 && SELL_SPLIT) {   // T coarse level: prolongate into r (free here), then sweep
+      launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.r.p,
+             SliceSkip{nullptr, nullptr, 1}, RowRange{0, lv.n});
+      launch(d, k_post<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p, (const double*)lv.b.p,
+             om, (const double*)lv.r.p, out, RowRange{0, lv.n});
     } else {
       launch(d, k_up<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, skip_at(l));

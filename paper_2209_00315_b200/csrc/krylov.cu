@@ -246,6 +246,20 @@ __global__ void k_gm_neg_norm(const double* __restrict__ a, double* __restrict__
   if (seg_commit<1>(acc, 1, A, s, out)) epi(out);
 }
 
+// ||a||  (no write)
+__global__ void k_gm_norm(const double* __restrict__ a, SegArgs A, EpiNorm epi) {
+  int s;
+  long long beg, end;
+  seg_chunk(A, s, beg, end);
+  double acc[1] = {0.0};
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    double v = a[i];
+    acc[0] += v * v;
+  }
+  __shared__ double out[1];
+  if (seg_commit<1>(acc, 1, A, s, out)) epi(out);
+}
+
 // V[j] = w / s and vin = V[j], s = beta (start) or hn (Arnoldi), only if the inner loop continues
 __global__ void k_gm_scale(long long nl, const double* __restrict__ w, double* __restrict__ V,
                            double* __restrict__ vin, const GmresScal* G, int start, SegArgs A) {
@@ -425,6 +439,15 @@ void DevGmres::reset_total(Dev& d) { launch(d, k_gm_reset_total, dim3(1), dim3(1
 void DevGmres::neg_norm(Dev& d, const double* a, double* b, double* norm) {
   const bool fused = comm == nullptr;
   launch(d, k_gm_neg_norm, dim3(parts, set.owned()), dim3(BS), 0, a, b, seg(fused ? 1 : 0), EpiNorm{norm});
+  if (!fused) {
+    allgather_tot(d);
+    launch(d, k_seg_finish<EpiNorm>, dim3(1), dim3(BS), 0, seg(0), 1, EpiNorm{norm});
+  }
+}
+
+void DevGmres::norm(Dev& d, const double* a, double* norm) {
+  const bool fused = comm == nullptr;
+  launch(d, k_gm_norm, dim3(parts, set.owned()), dim3(BS), 0, a, seg(fused ? 1 : 0), EpiNorm{norm});
   if (!fused) {
     allgather_tot(d);
     launch(d, k_seg_finish<EpiNorm>, dim3(1), dim3(BS), 0, seg(0), 1, EpiNorm{norm});

@@ -104,6 +104,8 @@ struct DevGmres {
             const double* scale, double tol, int maxit);
   // b = -a and *norm = ||a||_2 on this instance's slice set (the inner GMRES right-hand side)
   void neg_norm(Dev& d, const double* a, double* b, double* norm);
+  // *norm = ||a||_2 on this instance's slice set
+  void norm(Dev& d, const double* a, double* norm);
   void reset_total(Dev& d);
   void allgather_tot(Dev& d);
 };

@@ -146,6 +146,11 @@ static void prepare(bbot_ctx* c) {
   if (!c->nrm_T.p) c->nrm_T.alloc(4, c->dev.stream);
 }
 
+// A43: the T-solve's stopping scale, s = max(||r2||, (delta / eps_T) ||r||) (nrm[0] = ||r2||,
+// nrm[1] = ||r||, out nrm[2]); target = eps_T s
+constexpr double BB_T_NOISE = 1e-12;
+__global__ void k_bb_tscale(double* nrm, double ratio) { nrm[2] = fmax(nrm[0], ratio * nrm[1]); }
+
 // a4: z = BB(r), r = (r1; r2), z = (x; y)  ((4.18)-(4.20), (4.26), A9, A12, A14)
 static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   const bbot_solver_opts& o = c->opts;
@@ -154,9 +159,13 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
   const double* r2 = r + n;
   double* z1 = z;
   double* z2 = z + n;
-  // (i) T z2 = -r2, GMRES(restart_T) right-preconditioned by one AMG(T) V-cycle, relative eps_T
+  // (i) T z2 = -r2, GMRES(restart_T) right-preconditioned by one AMG(T) V-cycle, stopping at
+  //     max(eps_T ||r2||, delta ||r||) (A43: an r2 at rounding level of r -- P g~ at the A19
+  //     point, zero in exact arithmetic -- is not solved to eps_T relative)
   (void)m;
+  c->outer.norm(c->dev, r, c->nrm_T.p + 1);
   c->innerT.neg_norm(c->dev, r2, c->tmp_m.p, c->nrm_T.p);
+  launch(c->dev, k_bb_tscale, dim3(1), dim3(1), 0, c->nrm_T.p, BB_T_NOISE / o.eps_T);
   SliceEllView vT = view_T(c);
   c->innerT.emit(
       c->dev, c->red, [&](const double* x, double* y) { apply_T(c, x, y); },
@@ -164,7 +173,7 @@ static void emit_bb_apply(bbot_ctx* c, const double* r, double* z) {
         if (c->slab()) amg_vcycle_slab(c->dev, c->amgT, vT, x, y, *c->comm, c->ra(), c->rb());
         else amg_vcycle(c->dev, c->amgT, vT, x, y);
       },
-      c->tmp_m.p, c->tmp_m2.p, c->nrm_T.p, o.eps_T, o.maxit_inner);
+      c->tmp_m.p, c->tmp_m2.p, c->nrm_T.p + 2, o.eps_T, o.maxit_inner);
   // (ii) y = P^T Mbar^-1 Atilde z   (A12)
   bb_y_from_z(c, c->tmp_m2.p, z2);
   // (iii) b = r1 - B^T P^T y, slice means removed (compatibility)

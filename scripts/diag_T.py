@@ -45,6 +45,28 @@ def main(name):
         print("apply seed", seed, "T its gpu", itT, "oracle", S.inner_T_its, "A max gpu", itA,
               "oracle", int(S.inner_A_its[-1].max()), "rel", float(np.max(np.abs(zg - zo)) / np.max(np.abs(zo))))
 
+    # restarted T-GMRES(10): a tight inner tolerance forces restarts
+    o = pb.default_solver_opts(eps_T=1e-4)
+    ctx.set_opts(o)
+    ctx.assemble()
+    S2 = BBSolver(d, phi, rho, s, 1.0, SolverOpts(eps_T=1e-4))
+    for seed in range(2):
+        r = np.random.default_rng(seed).standard_normal(d.n + d.m)
+        r[d.n:] = d.P(r[d.n:])
+        S2.inner_T_its = 0
+        zg, itT, itA = ctx.bb_apply(r)
+        zo = S2.apply(r)
+        print("eps_T=1e-4 apply seed", seed, "T its gpu", itT, "oracle", S2.inner_T_its,
+              "rel", float(np.max(np.abs(zg - zo)) / np.max(np.abs(zo))))
+    ctx.set_opts(pb.default_solver_opts())
+    ctx.assemble()
+    dphi, drho, ds, st = ctx.solve()
+    S.inner_T_its = 0
+    S.inner_A_its = []
+    S.solve()
+    print("solve gpu", {k: st[k] for k in ("outer_its", "inner_T_its", "inner_A_its_max", "inner_A_its_total")},
+          "oracle", S.stats)
+
 
 if __name__ == "__main__":
     main(sys.argv[1] if len(sys.argv) > 1 else "C2")

@@ -316,3 +316,28 @@ def test_direct_newton_is_the_least_squares_min_norm_solution():
         rp = (rp - (rp[0] @ d.M) / d.area).reshape(-1)
         for a, b in ((dphi, rp), (drho, ref[n:n + m]), (ds, ref[n + m:])):
             assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_T_solve_noise_floor():
+    """A43: the T-solve of a BB apply stops at max(eps_T ||r2||, 1e-12 ||r||).  At the A19
+    point P g~ is zero in exact arithmetic (g~ is proportional to c̄ per slice); rounding-level
+    perturbations of r2 then cost no T iterations and leave z unchanged to rounding, while an
+    r2 well above the floor is solved to eps_T relative as before."""
+    p = make_problem("T1")
+    d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    phi, rho, s = initial_state(p, 1.0)
+    S = BBSolver(d, phi, rho, s, 1.0)
+    r = S.rhs / np.linalg.norm(S.rhs)
+    assert np.linalg.norm(r[d.n:]) <= 1e-14          # P g~ = 0 up to rounding
+    rng = np.random.default_rng(0)
+    z0 = S.apply(r)
+    t0 = S.inner_T_its
+    rn = r.copy()
+    rn[d.n:] += d.P(rng.standard_normal(d.m)) * 1e-15 / np.sqrt(d.m)
+    z1 = S.apply(rn)
+    assert S.inner_T_its == t0                       # noise: no T iterations
+    assert np.linalg.norm(z1 - z0) <= 1e-10 * np.linalg.norm(z0)
+    rs = r.copy()
+    rs[d.n:] += d.P(rng.standard_normal(d.m)) * 1e-6
+    S.apply(rs)
+    assert S.inner_T_its > t0                        # a real r2 is solved
