@@ -167,7 +167,7 @@ class ByteModel:
             return None
         base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
         a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView>" in base
-        if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict"):
+        if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict", "k_resid_sk<SellView>", "k_jacobi_sk"):
             lv = self._level(grid, by="nc" if base == "k_restrict" else "n")
             a_side = lv is not None and lv[0] == "A"
         return b * self.act if a_side else b
@@ -230,6 +230,15 @@ class ByteModel:
                 return None
             _, _, (nl, nnz, nc) = lv
             return 20 * nl + 8 * nc
+        if base in ("k_post<SellView>", "k_resid_sk<SellView>"):
+            lv = self._level(grid)
+            if lv is None:
+                return None
+            _, _, (nl, nnz, nc) = lv
+            return 12 * nnz + (32 * nl if base.startswith("k_post") else 24 * nl)
+        if base == "k_jacobi_sk":
+            lv = self._level(grid)
+            return 24 * lv[2][0] if lv else None
         if base == "k_jacobi0":
             lv = self._level(grid)
             return 24 * lv[2][0] if lv else None
@@ -245,11 +254,13 @@ class ByteModel:
             return 8 * m * (self.jT + 3)
         if base.startswith("k_gm_orth_dots"):
             return 8 * nm * (self.jO + 3)
-        if base.startswith("k_gm_orth<"):            # shared by both GMRES: launch-weighted mix
+        if base.startswith("k_gm_orth<12>"):         # T-GMRES: read V[0..j] w, write w
+            return 8 * m * (self.jT + 3)
+        if base.startswith("k_gm_orth<"):            # outer FGMRES
+            return 8 * nm * (self.jO + 3)
+        if base == "k_gm_scale":                     # both GMRES: read w, write V[j+1] vin (launch-weighted)
             wT, wO = self.its_T, self.its_O
-            return (wT * 8 * m * (self.jT + 3) + wO * 8 * nm * (self.jO + 3)) / max(1, wT + wO)
-        if base == "k_gm_scale":
-            return None
+            return (wT * 24 * m + wO * 24 * nm) / max(1, wT + wO)
         if base == "k_jp_y1":
             return 48 * n + 16 * N + 8 * (K + 1) * NE + 16 * m
         if base == "k_neg_norm":
@@ -602,6 +613,20 @@ def main():
     # per-launch profiler brackets every kernel with CUDA events on the launching
     # stream).  The eager issue runs exactly the kernels the graph replays
     # (bitwise-identical results), so its launch count is the step's launch count.
+    # ---- device memory of this context (the library's private pool; nothing else allocated from
+    # it yet): the FGMRES basis, divided by P under time slabs, and the rest (replicated)
+    mem = None
+    try:
+        used, peak = ctx.mem_usage()
+        r_out = 30
+        basis = (2 * r_out + 1) * (ctx.n + ctx.m) * 8 / world
+        mem = {"used_gb": round(used / 1e9, 3), "peak_gb": round(peak / 1e9, 3),
+               "fgmres_basis_gb": round(basis / 1e9, 3),
+               "other_gb": round((peak - basis) / 1e9, 3),
+               "note": "pool high-water mark after assemble + solve; the FGMRES(30) basis (61 vectors of "
+                       "n+m doubles) is slab-local (divided by P), the rest is replicated on every rank"}
+    except Exception as ex:
+        mem = {"error": str(ex)[:120]}
     roof = None
     kernels = None
     launches = None
@@ -664,6 +689,7 @@ def main():
             "e2e": {"value": e2e_steps / te, "unit": "solves/s", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
             "gpu_launches": int(launches) if launches is not None else None,
+            "memory": mem,
             "timing": {k: round(st[k], 3) for k in ("t_assemble_ms", "t_setup_ms", "t_krylov_ms", "t_graph_ms")},
             "ms_per_outer": round(st["t_krylov_ms"] / max(1, st["outer_its"]), 3),
             "roofline": roof,

@@ -244,10 +244,16 @@ bbot_status bbot_amg_vcycle(bbot_ctx* ctx, int which, const double* b, double* x
  * (kernels replayed from the solve's CUDA graph are not counted; run the same
  * solve with bbot_set_exec_mode(ctx, 0) or under the profiler to count them). */
 long long bbot_launch_count(const bbot_ctx* ctx);
+/* Device memory of the library's private stream-ordered pool on the context's device (every
+ * bbot buffer -- state, assembly, AMG hierarchies, Krylov workspaces -- is allocated from it;
+ * contexts of one process on one device share the pool): *used_bytes = currently allocated,
+ * *peak_bytes = high-water mark since the pool was created.  BBOT_E_INPUT on NULL. */
+bbot_status bbot_mem_usage(const bbot_ctx* ctx, long long* used_bytes, long long* peak_bytes);
 /* Multi-GPU time slabs ("well suited for
- * parallelization"), one rank per GPU.  Rank r owns the potential slices [k_begin, k_end)
- * = [floor(r(K+1)/P), floor((r+1)(K+1)/P)) and the density slices [k_begin, min(k_end, K));
- * 2P <= K+1.  The Newton SOLVE is decomposed: the FGMRES and T-GMRES Krylov vectors, J_P
+ * parallelization"), one rank per GPU.  Rank r owns whole AMG(T) time blocks (bbot_time_blocks:
+ * B = max(1, floor(K/8)) slices, nb = floor(K/B) blocks): the potential slices [k_begin, k_end),
+ * k_begin = B floor(r nb / P) (k_end of the last rank = K+1), and the density slices
+ * [k_begin, min(k_end, K)); P <= nb.  The Newton SOLVE is decomposed: the FGMRES and T-GMRES Krylov vectors, J_P
  * (4.17), the T-solve (T SpMV and every grid-wide level of the AMG(T) V-cycle), the BB glue
  * (4.18)-(4.20), the per-slice A_k PCG solves and the recovery (a6) run on the owned slices,
  * with one-slice halo exchanges (x1 from the right and x2, y from the left for J_P, B, B^T;

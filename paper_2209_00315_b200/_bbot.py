@@ -100,6 +100,7 @@ _sigs = {
     "bbot_amg_level_info": (C.c_int, [_P, C.c_int, C.c_int] + [C.POINTER(C.c_longlong)] * 3 + [C.POINTER(C.c_int)]),
     "bbot_amg_vcycle": (C.c_int, [_P, C.c_int, _P, _P, C.c_int]),
     "bbot_launch_count": (C.c_longlong, [_P]),
+    "bbot_mem_usage": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "bbot_set_exec_mode": (C.c_int, [_P, C.c_int]),
     "bbot_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "bbot_set_dist": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
@@ -373,6 +374,12 @@ class Context:
 
     def launch_count(self):
         return lib.bbot_launch_count(self._h)
+
+    def mem_usage(self):
+        """(used, peak) bytes of the library's device memory pool (bbot_mem_usage)."""
+        u, pk = C.c_longlong(), C.c_longlong()
+        self._check(lib.bbot_mem_usage(self._h, C.byref(u), C.byref(pk)))
+        return u.value, pk.value
 
     def set_dist(self, rank: int, nranks: int, uid: bytes | None):
         """Time-slab decomposition over NCCL (uid: 128 bytes from nccl_unique_id() on rank 0)."""

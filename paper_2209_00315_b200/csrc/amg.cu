@@ -340,6 +340,23 @@ __global__ void k_resid(V v, const double* __restrict__ b, const double* __restr
   res[r] = acc;
 }
 
+// coarse levels, split pre-smoothing (BBOT_DOWN_SPLIT): x = om D^-1 b, then r = b - A x with one
+// gather per entry instead of k_down's two (dinv[c], b[c]); the same values (bitwise)
+__global__ void k_jacobi_sk(long long n, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                            double* __restrict__ x, SliceSkip sk) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n && !sk.skip(r)) x[r] = om * dinv[r] * b[r];
+}
+template <class V>
+__global__ void k_resid_sk(V v, const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ res,
+                           SliceSkip sk) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= v.nrows || sk.skip(r)) return;
+  double acc = b[r];
+  v.row(r, [&](long long c, double a) { acc -= a * x[c]; });
+  res[r] = acc;
+}
+
 // xp = x + P xc (prolongated coarse correction), then the post-smoothing sweep on xp:
 // two launches instead of k_up's chained gathers (neighbour -> agg -> xc) on each of
 // T's ~27 entries per row; the same sums in the same order (bitwise identical)
@@ -524,7 +541,8 @@ static const long long TAIL_ROWS = tune_env("BBOT_TAIL_ROWS", 0);       // A-tai
 static const long long TAILT_ROWS = tune_env("BBOT_TAILT_ROWS", 16384); // first T-tail level: <= rows in total
 static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tail cluster size (0: 148/slices)
 static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
-static const bool SELL_SPLIT = tune_env("BBOT_SELL_SPLIT", 0) != 0;    // T coarse levels: prolong + post
+static const bool SELL_SPLIT = tune_env("BBOT_SELL_SPLIT", 1) != 0;    // T coarse levels: prolong + post
+static const bool DOWN_SPLIT = tune_env("BBOT_DOWN_SPLIT", 0) != 0;    // coarse levels: jacobi + resid
 static const int TAILA_THREADS = (int)tune_env("BBOT_TAILA_BS", 1024);   // k_tailA block size (<= TAIL_BS)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
@@ -1401,7 +1419,12 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     } else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
              RowRange{0, lv.n});
-    else
+    else if (DOWN_SPLIT) {
+      launch(d, k_jacobi_sk, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, (const double*)lv.b.p, om,
+             lv.x.p, skip_at(l));
+      launch(d, k_resid_sk<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.b.p, (const double*)lv.x.p,
+             lv.r.p, skip_at(l));
+    } else
       launch(d, k_down<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
              (const double*)lv.b.p, om, lv.x.p, lv.r.p, skip_at(l), RowRange{0, lv.n});
     if (!(H.tail > 0 && l == stop - 1))

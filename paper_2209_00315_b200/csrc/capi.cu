@@ -522,6 +522,22 @@ bbot_status bbot_amg_vcycle(bbot_ctx* c, int which, const double* b, double* x, 
 
 long long bbot_launch_count(const bbot_ctx* c) { return c ? c->dev.launches : 0; }
 
+bbot_status bbot_mem_usage(const bbot_ctx* c, long long* used_bytes, long long* peak_bytes) {
+  if (!c || !used_bytes || !peak_bytes) return BBOT_E_INPUT;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->devid);
+  cudaMemPool_t pool = bbot::device_pool();
+  unsigned long long used = 0, high = 0;   // cuuint64_t
+  cudaError_t e1 = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  cudaError_t e2 = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high);
+  cudaSetDevice(prev);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return BBOT_E_CUDA;
+  *used_bytes = (long long)used;
+  *peak_bytes = (long long)high;
+  return BBOT_OK;
+}
+
 bbot_status bbot_nccl_unique_id(unsigned char out[128]) {
   if (!out) return BBOT_E_INPUT;
   try {
