@@ -6,6 +6,7 @@ tests/test_gpu_parity.py::test_ipm_parity_C1_full compares the CUDA path to it (
 oracle needs ~10 min on one core for C1, too long to re-run inside the GPU suite).
 
     python scripts/oracle_ipm_golden.py C1
+    python scripts/oracle_ipm_golden.py C2 0.0078125     # mu 1 -> 2^-7 only (-> ipm_C2_mu7.json)
 """
 import json
 import os
@@ -22,7 +23,7 @@ from oracle.ops import Discretisation  # noqa: E402
 from synthetic import initial_state, make_problem  # noqa: E402
 
 
-def main(name):
+def main(name, mu_min=None):
     p = make_problem(name)
     d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     phi, rho, s = initial_state(p, 1.0)
@@ -36,14 +37,17 @@ def main(name):
         print(log[-1], f"{time.time() - t0:.0f}s", flush=True)
 
     with threadpool_limits(1):
-        res = ipm_run(d, phi, rho, s, IpmOpts(), SolverOpts(), callback=cb)
-    out = {"config": name, "kinetic_energy": res.kinetic_energy, "final_mu": res.mu, "n_systems": len(log),
+        opts = IpmOpts() if mu_min is None else IpmOpts(mu_min=mu_min)
+        res = ipm_run(d, phi, rho, s, opts, SolverOpts(), callback=cb)
+    out = {"config": name, "mu_min": mu_min, "kinetic_energy": res.kinetic_energy, "final_mu": res.mu,
+           "n_systems": len(log),
            "seconds_1core": round(time.time() - t0, 1), "opts": SolverOpts().__dict__, "systems": log,
            "note": "oracle full IPM (A17-A20), written by scripts/oracle_ipm_golden.py (oracle/ only)"}
-    path = os.path.join(ROOT, "tests", "golden", f"ipm_{name}.json")
+    tag = "" if mu_min is None else f"_mu{round(-__import__('math').log2(mu_min))}"
+    path = os.environ.get("ORACLE_IPM_OUT") or os.path.join(ROOT, "tests", "golden", f"ipm_{name}{tag}.json")
     json.dump(out, open(path, "w"), indent=0)
     print("wrote", path, "KE", res.kinetic_energy)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "C1")
+    main(sys.argv[1] if len(sys.argv) > 1 else "C1", float(sys.argv[2]) if len(sys.argv) > 2 else None)

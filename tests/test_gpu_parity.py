@@ -303,6 +303,28 @@ def test_ipm_parity_C1_full():
     _ipm_compare(log, gold["systems"], st, gold["kinetic_energy"])
 
 
+def test_ipm_parity_C2_to_mu7():
+    """BASELINE configs[1] (C2: 8192 cells on the jittered mesh, K = 32, 1.07 M unknowns, the
+    AMG(T) time blocks of A42 active) over its first seven mu values, mu 1 -> 2^-7 (A17-A20),
+    against the oracle's own run stored in tests/golden/ipm_C2_mu7.json
+    (scripts/oracle_ipm_golden.py C2 0.0078125, oracle only; ~1 h on one core): same
+    systems, trajectory, kinetic energy to 1e-6."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "ipm_C2_mu7.json")
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated")
+    gold = json.load(open(path))
+    pb = _gpu()
+    p = make_problem("C2")
+    phi, rho, s = initial_state(p, 1.0)
+    ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
+    ctx.set_state(phi, rho, s, 1.0)
+    st, log = ctx.ipm_run(pb.default_ipm_opts(mu_min=gold["mu_min"]))
+    assert abs(st["final_mu"] - gold["final_mu"]) <= 1e-15 * gold["final_mu"]
+    _ipm_compare(log, gold["systems"], st, gold["kinetic_energy"])
+
+
 def test_ipm_parity_C1_converging_range():
     """IPM on BASELINE configs[0] (C1: 512 cells, K = 8) over the mu range where the
     BB-preconditioned FGMRES converges, mu 1 -> 2^-9 ~ 1.95e-3 (A17-A20; 36 Newton
