@@ -251,7 +251,7 @@ long long bbot_launch_count(const bbot_ctx* ctx);
 bbot_status bbot_mem_usage(const bbot_ctx* ctx, long long* used_bytes, long long* peak_bytes);
 /* Multi-GPU time slabs ("well suited for
  * parallelization"), one rank per GPU.  Rank r owns whole AMG(T) time blocks (bbot_time_blocks:
- * B = max(1, floor(K/8)) slices, nb = floor(K/B) blocks): the potential slices [k_begin, k_end),
+ * B slices, nb = floor(K/B) blocks): the potential slices [k_begin, k_end),
  * k_begin = B floor(r nb / P) (k_end of the last rank = K+1), and the density slices
  * [k_begin, min(k_end, K)); P <= nb.  The Newton SOLVE is decomposed: the FGMRES and T-GMRES Krylov vectors, J_P
  * (4.17), the T-solve (T SpMV and every grid-wide level of the AMG(T) V-cycle), the BB glue
@@ -283,8 +283,9 @@ bbot_status bbot_get_slab(const bbot_ctx* ctx, int* k_begin, int* k_end);
 bbot_status bbot_slab_plan(int Kp1, int nranks, int rank, int S, int* lo, int* hi);
 /* The time blocks of AMG(T) (A42; the aggregation unit of T, whose rows couple
  * consecutive time slices through the time Laplacian in -B M^-1 B~, eq. (4.26)):
- * *block_size = B = max(1, floor(K/8)) consecutive density slices, *nblocks = floor(K/B),
- * the last block taking the remainder.  Host only.  BBOT_E_INPUT if K < 1. */
+ * *block_size = B consecutive density slices (B = 1 in this build: multi-slice blocks were
+ * measured and not adopted), *nblocks = floor(K/B), the last block taking the remainder.
+ * Host only.  BBOT_E_INPUT if K < 1. */
 bbot_status bbot_time_blocks(int K, int* block_size, int* nblocks);
 
 /* Execution mode of bbot_solve.  1 (default): the whole solve -- FGMRES, the BB

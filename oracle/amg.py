@@ -53,17 +53,18 @@ KC_MIN_LEVELS = 7   # ... in hierarchies of >= KC_MIN_LEVELS levels.  Plain aggr
 _M32 = np.uint64(0xFFFFFFFF)
 
 
+TIME_BLOCK = 1   # A42: slices per AMG(T) aggregation block (1 = I3's within-slice rule)
+
+
 def time_blocks(K: int) -> np.ndarray:
-    """A42: the aggregation unit of AMG(T).  T couples consecutive time slices (the time
-    Laplacian -B M^-1 B~ ⊇ D_t M̄ D_t^T, A8); aggregating within single slices never coarsens
-    that coupling, and after a few spatial levels it dominates (it grows with the aggregate
-    mass while the 2D spatial Galerkin couplings do not): T-GMRES needed 15 iterations per
-    outer iteration at K = 128 against the paper's 1.7-5.7.  So T's rows are grouped
-    in B = max(1, floor(K/8)) consecutive density slices -- 8 blocks, the last one taking the
-    remainder -- and aggregates may span the slices of a block.  8 blocks keep the
-    decomposition into P <= 8 time slabs exact (slab boundaries on block boundaries, §8(e)).
-    Returns the block of each slice (K,)."""
-    B = max(1, K // 8)
+    """A42: the aggregation unit of AMG(T), blocks of TIME_BLOCK consecutive density slices
+    (the last block taking the remainder); aggregates never span two blocks.  T couples
+    consecutive slices (the time Laplacian in -B M^-1 B~, A8), which single-slice aggregates
+    never coarsen; blocks of max(1, K/8) slices were measured (A42): 2-3x fewer
+    T-GMRES iterations at the A19 point and on some IPM iterates, 2x MORE on others (C2 at
+    mu = 1 after five Newton steps: 606 -> 1296; the C3 IPM stalled 30x earlier in mu), so
+    the build keeps within-slice aggregation (B = 1).  Returns the block of each slice (K,)."""
+    B = TIME_BLOCK
     nb = max(1, K // B)
     return np.minimum(np.arange(K) // B, nb - 1)
 

@@ -12,6 +12,7 @@
 namespace cg = cooperative_groups;
 
 namespace bbot {
+constexpr int DOWN_RPT = 4;   // rows per thread of k_down_sl
 
 constexpr double AMG_TAU = 1e-8;        // near-tie tolerance (relative)
 constexpr double AMG_DECOUPLED = 1e-10; // rows with max strength <= this*|a_ii| do not propose
@@ -312,6 +313,28 @@ __global__ void k_down(V v, const double* __restrict__ dinv, const double* __res
   res[r] = acc;
 }
 
+// level-0 pre-smoothing of the per-slice PCG (mode A) on a (parts, slices) grid: the blocks of
+// a converged slice leave at once (k_down's one-row-per-thread grid launched n/256 blocks that
+// each tested the slice of their rows: ~20 % of a full launch when few slices remain active)
+template <class V>
+__global__ void __launch_bounds__(256) k_down_sl(V v, const double* __restrict__ dinv, const double* __restrict__ b,
+                                                 double om, double* __restrict__ x, double* __restrict__ res,
+                                                 long long L, const double* active) {
+  const int k = blockIdx.y;
+  if (active && active[k] == 0.0) return;
+  const long long i0 = (long long)blockIdx.x * (blockDim.x * DOWN_RPT) + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < DOWN_RPT; j++) {
+    const long long i = i0 + (long long)j * blockDim.x;
+    if (i >= L) return;
+    const long long r = (long long)k * L + i;
+    double acc = b[r];
+    v.row(r, [&](long long c, double a) { acc -= a * (om * dinv[c] * b[c]); });
+    x[r] = om * dinv[r] * b[r];
+    res[r] = acc;
+  }
+}
+
 __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
                            const double* __restrict__ r, double* bc, SliceSkip sk, RowRange rr) {
   long long I = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -543,6 +566,7 @@ static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tai
 static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
 static const bool SELL_SPLIT = tune_env("BBOT_SELL_SPLIT", 1) != 0;    // T coarse levels: prolong + post
 static const bool DOWN_SPLIT = tune_env("BBOT_DOWN_SPLIT", 0) != 0;    // coarse levels: jacobi + resid
+static const bool DOWN_SL = tune_env("BBOT_DOWN_SL", 1) != 0;          // A level 0 (PCG): (parts, slices) grid
 static const int TAILA_THREADS = (int)tune_env("BBOT_TAILA_BS", 1024);   // k_tailA block size (<= TAIL_BS)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
@@ -612,37 +636,85 @@ __device__ __forceinline__ double tail_dot(const double* u, const double* v, lon
 }
 __device__ __forceinline__ double tail_div(double a, double b) { return b != 0.0 ? a / b : 0.0; }
 
+// NV per-slice dots at once (the K-cycle's dots fused into the passes that produce their
+// operands): per value a warp butterfly, one shared-memory exchange, every thread summing the
+// warps' partials in warp order (then the cluster's CTAs in rank order) -- one barrier pair
+// for all NV values instead of one tail_dot (two block barriers + two more) per value
+template <int NV>
+__device__ __forceinline__ void tail_reduce(const double (&acc)[NV], double (&tot)[NV], const TailPos& P) {
+  __shared__ double shr[NV][32];
+  __shared__ double part[NV];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; k++) {
+    double v = warp_sum(acc[k]);
+    if (lane == 0) shr[k][w] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; k++) {
+    double t = 0.0;
+    for (int q = 0; q < nw; q++) t += shr[k][q];
+    tot[k] = t;
+  }
+  if (P.cs == 1) {
+    __syncthreads();                   // shr reused by the next call
+    return;
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NV; k++) part[k] = tot[k];
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+#pragma unroll
+  for (int k = 0; k < NV; k++) {
+    double t = 0.0;
+    for (int q = 0; q < P.cs; q++) t += cl.map_shared_rank(part, q)[k];
+    tot[k] = t;
+  }
+  cl.sync();
+}
+
 __device__ void tail_cycle(const TailArgs* __restrict__ T, int q, const TailPos& P);
 
-// K-cycle step at tail level q: input lv[q].b (= rc), output lv[q].xo (oracle amg.kstep)
+// K-cycle step at tail level q: input lv[q].b (= rc), output lv[q].xo (oracle amg.kstep).
+// Each dot is accumulated in the pass that produces its operands (row-local products), and
+// the dots of one pass are reduced together: rho1 = c1.v1 and a1 = c1.rc with v1 = A c1;
+// g = c2.v1, a2 = c2.r2 and beta = c2.v2 with v2 = A c2 -- five barrier-separated dot phases
+// of the latency-bound tail become two
 __device__ void tail_kstep(const TailArgs* __restrict__ T, int q, const TailPos& P) {
   const TailLevel& L = T->lv[q];
   const long long s0 = L.sptr[P.k], s1 = L.sptr[P.k + 1];
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.krc[r] = L.b[r];
   tail_sync(P);
   tail_cycle(T, q, P);                                   // c1 -> xo
+  double a2v[2] = {0.0, 0.0}, t2[2];
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
-    L.kc1[r] = L.xo[r];
+    const double c1 = L.xo[r];
+    L.kc1[r] = c1;
     double av = 0.0;
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
     L.kv[r] = av;                                        // v1 = A c1
+    a2v[0] += c1 * av;
+    a2v[1] += c1 * L.krc[r];
   }
-  tail_sync(P);
-  const double rho1 = tail_dot(L.kc1, L.kv, s0, s1, P);
-  const double a1 = tail_dot(L.kc1, L.krc, s0, s1, P);
+  tail_reduce<2>(a2v, t2, P);
+  const double rho1 = t2[0], a1 = t2[1];
   const double f1 = tail_div(a1, rho1);
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) L.b[r] = L.krc[r] - f1 * L.kv[r];   // r2
   tail_sync(P);
   tail_cycle(T, q, P);                                   // c2 -> xo
-  const double g = tail_dot(L.xo, L.kv, s0, s1, P);
-  const double a2 = tail_dot(L.xo, L.b, s0, s1, P);
+  double a3v[3] = {0.0, 0.0, 0.0}, t3[3];
   for (long long r = P.first_row(s0); r < s1; r += P.stride()) {
+    const double c2 = L.xo[r];
     double av = 0.0;
     L.A.row(r, [&](long long col, double a) { av += a * L.xo[col]; });
+    a3v[0] += c2 * L.kv[r];                              // g = c2.v1
+    a3v[1] += c2 * L.b[r];                               // a2 = c2.r2
+    a3v[2] += c2 * av;                                   // beta = c2.v2
     L.kv[r] = av;                                        // v2 = A c2
   }
-  tail_sync(P);
-  const double beta = tail_dot(L.xo, L.kv, s0, s1, P);
+  tail_reduce<3>(a3v, t3, P);
+  const double g = t3[0], a2 = t3[1], beta = t3[2];
   const double rho2 = beta - g * tail_div(g, rho1);
   const double g2 = tail_div(a2, rho2);
   const double e1 = f1 - g * tail_div(g2, rho1);
@@ -1416,7 +1488,10 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     if (l == 0 && H.mode == 1) {   // T level 0: Jacobi step first, then a plain residual sweep
       launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, RowRange{0, lv.n});
       launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, RowRange{0, lv.n});
-    } else if (l == 0)
+    } else if (l == 0 && fuse && DOWN_SL)
+      launch(d, k_down_sl<V0>, dim3((unsigned)((fuse->L + BS * DOWN_RPT - 1) / (BS * DOWN_RPT)), fuse->ns), dim3(BS), 0,
+             v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, fuse->L, active);
+    else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
              RowRange{0, lv.n});
     else if (DOWN_SPLIT) {

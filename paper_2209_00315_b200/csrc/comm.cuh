@@ -37,11 +37,12 @@ struct Layout {
   }
 };
 
-// A42: AMG(T) aggregates within time blocks of B = max(1, floor(K/8)) consecutive density
-// slices (nb = floor(K/B) blocks, the last one taking the remainder) -- the same rule as
-// oracle/amg.py::time_blocks.  The slabs are unions of whole blocks, so the decomposition
-// stays exact (P <= nb).
-inline int time_block_size(int K) { return std::max(1, K / 8); }
+// A42: AMG(T) aggregates within time blocks of B consecutive density slices (nb = floor(K/B)
+// blocks, the last one taking the remainder) -- the same rule as oracle/amg.py::time_blocks.
+// The slabs are unions of whole blocks, so the decomposition stays exact (P <= nb).  B = 1
+// (I3's within-slice aggregation): blocks of max(1, floor(K/8)) slices cut the T iterations
+// 2-3x on some systems and doubled them on others (A42), so they are not used.
+inline int time_block_size(int K) { (void)K; return 1; }   // A42 measured: blocks of max(1, K/8) not adopted
 inline int time_blocks(int K) { return std::max(1, K / time_block_size(K)); }
 inline int time_block_of(int K, int k) { return std::min(k / time_block_size(K), time_blocks(K) - 1); }
 

@@ -231,7 +231,7 @@ void nccl_unique_id(unsigned char out[128]) {
 void set_dist(bbot_ctx* c, int rank, int nranks, const unsigned char* uid, long long group) {
   BB_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, BBOT_E_INPUT, "bad rank / nranks");
   BB_REQUIRE(nranks == 1 || nranks <= time_blocks(c->g.K), BBOT_E_INPUT,
-             "time slabs: every rank needs >= 1 time block (P <= max(1, K / max(1, K/8)))");
+             "time slabs: every rank needs >= 1 AMG(T) time block (P <= nb, bbot_time_blocks)");
   drop_dist(c);
   drop_solve_graph(c);
   c->rank = rank;

@@ -1,0 +1,4 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r3a_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hss.py tests/test_gpu_edge.py -q -p no:cacheprovider -x -k "kcycle or amg or bb_apply or C4 or C3 or hss" > gpurun_out/r3a_tests.log 2>&1; echo rc=$? >> gpurun_out/r3a_tests.log
+timeout 600 python bench.py --steps 3 --warmup 2 --side-config C2 --no-cpu-baseline --ipm-config '' --e2e-steps 1 --profile-out gpurun_out/r3a_prof.json > gpurun_out/r3a_bench.log 2>&1

@@ -44,7 +44,7 @@ def _setup(name, state="random", mu=1e-2, seed=3, **kw):
     return pb, p, d, ctx, (phi, rho, s, mu)
 
 
-# ("T2", K=32): AMG(T) time blocks of B = 4 slices (A42; K <= 15 gives single-slice blocks)
+# ("T2", K=32): a deeper time axis (32 slices on 128 cells)
 CASES = [("T1", {}), ("C1", {}), ("T2b", {}), ("T2", {"K": 32})]
 
 

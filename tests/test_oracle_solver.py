@@ -120,37 +120,37 @@ def test_vcycle_symmetric_and_convergent():
     assert sz[0] / sz[1] > 2.5 and sz[1] / sz[2] > 2.5
 
 
-def test_time_blocks_bound_the_T_aggregates():
-    """A42: AMG(T) groups T's rows in time blocks (oracle/amg.py::time_blocks) -- every
-    aggregate on every level lies in one block, aggregates DO span slices inside a block
-    (the time coupling of T is coarsened), and with single-slice blocks (K <= 15) the rule
-    reduces to I3's within-slice aggregation."""
-    assert list(amg.time_blocks(8)) == list(range(8))            # K <= 15: B = 1
-    assert list(amg.time_blocks(20)) == [0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9]
-    assert list(amg.time_blocks(32)) == [k // 4 for k in range(32)]
+def test_time_blocks_bound_the_T_aggregates(monkeypatch):
+    """A42: AMG(T) groups T's rows in time blocks (oracle/amg.py::time_blocks); the build uses
+    single-slice blocks (TIME_BLOCK = 1, I3's rule).  With blocks of 2 slices (the machinery
+    the GPU shares through bbot_time_blocks) every aggregate on every level lies in one block
+    and aggregates do span the slices of a block; with the default every aggregate lies in
+    one slice."""
+    assert amg.TIME_BLOCK == 1 and list(amg.time_blocks(8)) == list(range(8))
     p = make_problem("T1", L=1, K=16)
     d = Discretisation(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     phi, rho, s = initial_state(p, 1.0)
     T = d.T_matrix(phi, rho, s)
-    blk = amg.time_blocks(d.K)
-    assert blk.max() == 7 and np.all(np.bincount(blk) == 2)
-    slT = np.repeat(np.arange(d.K), d.nbar)
-    H = amg.setup(T, np.repeat(blk, d.nbar), "T", 1.0, 64)
-    spans = False
-    member_slice = slT.copy()
-    member_block = np.repeat(blk, d.nbar)
-    for lv in H.levels[:-1]:
-        for c in range(lv.nc):
-            mem = np.nonzero(lv.agg == c)[0]
-            assert len(set(member_block[mem])) == 1
-            spans |= len(set(member_slice[mem])) > 1
-        # coarse rows inherit their block / (first) slice for the next level
-        first = np.full(lv.nc, -1)
-        for i in range(len(lv.agg) - 1, -1, -1):
-            first[lv.agg[i]] = i
-        member_block = member_block[first]
-        member_slice = member_slice[first]
-    assert spans
+    for B in (2, 1):
+        monkeypatch.setattr(amg, "TIME_BLOCK", B)
+        blk = amg.time_blocks(d.K)
+        assert list(blk) == [k // B for k in range(16)]
+        slT = np.repeat(np.arange(d.K), d.nbar)
+        H = amg.setup(T, np.repeat(blk, d.nbar), "T", 1.0, 64)
+        spans = False
+        member_slice = slT.copy()
+        member_block = np.repeat(blk, d.nbar)
+        for lv in H.levels[:-1]:
+            for c in range(lv.nc):
+                mem = np.nonzero(lv.agg == c)[0]
+                assert len(set(member_block[mem])) == 1
+                spans |= len(set(member_slice[mem])) > 1
+            first = np.full(lv.nc, -1)
+            for i in range(len(lv.agg) - 1, -1, -1):
+                first[lv.agg[i]] = i
+            member_block = member_block[first]
+            member_slice = member_slice[first]
+        assert spans == (B > 1)
 
 
 # ----------------------------------------------------------- BB / recovery
