@@ -12,7 +12,6 @@
 namespace cg = cooperative_groups;
 
 namespace bbot {
-constexpr int DOWN_RPT = 4;   // rows per thread of k_down_sl
 
 constexpr double AMG_TAU = 1e-8;        // near-tie tolerance (relative)
 constexpr double AMG_DECOUPLED = 1e-10; // rows with max strength <= this*|a_ii| do not propose
@@ -313,28 +312,6 @@ __global__ void k_down(V v, const double* __restrict__ dinv, const double* __res
   res[r] = acc;
 }
 
-// level-0 pre-smoothing of the per-slice PCG (mode A) on a (parts, slices) grid: the blocks of
-// a converged slice leave at once (k_down's one-row-per-thread grid launched n/256 blocks that
-// each tested the slice of their rows: ~20 % of a full launch when few slices remain active)
-template <class V>
-__global__ void __launch_bounds__(256) k_down_sl(V v, const double* __restrict__ dinv, const double* __restrict__ b,
-                                                 double om, double* __restrict__ x, double* __restrict__ res,
-                                                 long long L, const double* active) {
-  const int k = blockIdx.y;
-  if (active && active[k] == 0.0) return;
-  const long long i0 = (long long)blockIdx.x * (blockDim.x * DOWN_RPT) + threadIdx.x;
-#pragma unroll
-  for (int j = 0; j < DOWN_RPT; j++) {
-    const long long i = i0 + (long long)j * blockDim.x;
-    if (i >= L) return;
-    const long long r = (long long)k * L + i;
-    double acc = b[r];
-    v.row(r, [&](long long c, double a) { acc -= a * (om * dinv[c] * b[c]); });
-    x[r] = om * dinv[r] * b[r];
-    res[r] = acc;
-  }
-}
-
 __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
                            const double* __restrict__ r, double* bc, SliceSkip sk, RowRange rr) {
   long long I = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -566,7 +543,6 @@ static const int TAIL_CL = (int)tune_env("BBOT_TAIL_CL", 1);            // A-tai
 static const bool UP_SPLIT = tune_env("BBOT_UP_SPLIT", 0) != 0;        // A level 0: prolong + post_dot
 static const bool SELL_SPLIT = tune_env("BBOT_SELL_SPLIT", 1) != 0;    // T coarse levels: prolong + post
 static const bool DOWN_SPLIT = tune_env("BBOT_DOWN_SPLIT", 0) != 0;    // coarse levels: jacobi + resid
-static const bool DOWN_SL = tune_env("BBOT_DOWN_SL", 1) != 0;          // A level 0 (PCG): (parts, slices) grid
 static const int TAILA_THREADS = (int)tune_env("BBOT_TAILA_BS", 1024);   // k_tailA block size (<= TAIL_BS)
 constexpr int KC_ROWS = 4096;        // == oracle KC_ROWS
 constexpr int KC_MIN_LEVELS = 7;     // == oracle KC_MIN_LEVELS: K-cycle only in deep hierarchies
@@ -1488,10 +1464,7 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     if (l == 0 && H.mode == 1) {   // T level 0: Jacobi step first, then a plain residual sweep
       launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, RowRange{0, lv.n});
       launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, RowRange{0, lv.n});
-    } else if (l == 0 && fuse && DOWN_SL)
-      launch(d, k_down_sl<V0>, dim3((unsigned)((fuse->L + BS * DOWN_RPT - 1) / (BS * DOWN_RPT)), fuse->ns), dim3(BS), 0,
-             v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, fuse->L, active);
-    else if (l == 0)
+    } else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
              RowRange{0, lv.n});
     else if (DOWN_SPLIT) {
