@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import subprocess
 import sys
@@ -161,11 +162,19 @@ class ByteModel:
         if pcg_launches:
             self.act = min(1.0, st["inner_A_its_total"] / (pcg_launches * (self.K + 1)))
 
+    @staticmethod
+    def _base(name):
+        """Kernel name without arguments; the slice-batched level-0 kernels (k_*_sb / _sbx<NS, MINB>,
+        NS slices per block) move the bytes of the kernel they batch."""
+        base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
+        m = re.match(r"(k_pcg_pq|k_down|k_up_dot)_sbx?<", base)
+        return f"{m.group(1)}<LapView>" if m else base
+
     def bytes(self, name, grid):
         b = self._bytes(name, grid)
         if b is None:
             return None
-        base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
+        base = self._base(name)
         a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView>" in base
         if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict", "k_resid_sk<SellView>", "k_jacobi_sk"):
             lv = self._level(grid, by="nc" if base == "k_restrict" else "n")
@@ -192,7 +201,7 @@ class ByteModel:
     def _bytes(self, name, grid):
         n, m, N, K, NE = self.n, self.m, self.N, self.K, self.NE
         nm = n + m
-        base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
+        base = self._base(name)
         if base == "k_pcg_pq<LapView>":
             return 40 * n + self.lapA                 # read z p q, write p q (+ A in cell-ELL)
         if base == "k_pcg_xr":

@@ -5,6 +5,7 @@
 #include "amg.cuh"
 #include "comm.cuh"
 #include <climits>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <chrono>
 #include <memory>
@@ -428,6 +429,53 @@ __global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_up_dot(V v, const double
     dot += b[r] * z;
   }
   if (red_commit(dot, R)) fin(R.out);
+}
+
+// ---- slice-batched level-0 pre-smoothing (LapView).  The level-0 sweeps of AMG(A) are
+// latency-bound (ncu: ~85 % of warp samples in long-scoreboard stalls at full occupancy,
+// DRAM at ~51-55 % of peak).  k_down_sb's block (x, j) runs kites x*256.. of the NS = 2
+// slices 2j, 2j+1: each thread loads kite i's neighbour slots once (nb is shared by all
+// slices) and sweeps the rows kk*N + i of both slices -- the same rows and the same
+// expression order as k_down (bitwise identical).  Measured on C4: k_down<LapView> 721 ->
+// 624 ms per solve.  The same batching of k_up_dot / k_pcg_pq (2 or 4 slices, 4-8 CTAs per
+// SM) and an explicit all-loads-first variant of all three measured slower on C4 (k_up_dot
+// 929 -> 1107-3058 ms, k_pcg_pq 716 -> 770-1351 ms; profiles/r2z_ab_lap_sb_C4.log) and were
+// removed.
+int lap_sb() {
+  const char* e = getenv("BBOT_LAP_SB");
+  int v = e ? atoi(e) : 2;
+  return v == 2 ? 2 : 1;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256, 6) k_down_sb(LapView v, const double* __restrict__ dinv,
+                                                    const double* __restrict__ b, double om, double* __restrict__ x,
+                                                    double* __restrict__ res, const double* __restrict__ active,
+                                                    int ns) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k0 = blockIdx.y * NS;
+  if (i >= v.N) return;
+  int c[4];
+  v.nbrs(i, c);
+#pragma unroll
+  for (int s = 0; s < NS; s++) {
+    const int kk = k0 + s;
+    if (kk >= ns || (active && active[kk] == 0.0)) continue;
+    const long long r = (long long)kk * v.N + i;
+    double acc = b[r];
+    v.row_nb(kk, i, c, [&](long long cc, double a) { acc -= a * (om * dinv[cc] * b[cc]); });
+    x[r] = om * dinv[r] * b[r];
+    res[r] = acc;
+  }
+}
+
+// level 0 of an AMG(A) hierarchy on the plain cell-ELL view, slice-major rows of N
+template <class V0>
+static bool lap_batched(const V0& v0, const AmgHierarchy& H) {
+  if constexpr (std::is_same<V0, LapView>::value)
+    return lap_sb() > 1 && H.mode != 1 && H.nslices > 0 && (long long)v0.N * H.nslices == H.lv[0].n;
+  else
+    return false;
 }
 
 // ------------------------------------------------------------ coarsest
@@ -1464,6 +1512,10 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     if (l == 0 && H.mode == 1) {   // T level 0: Jacobi step first, then a plain residual sweep
       launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, RowRange{0, lv.n});
       launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, RowRange{0, lv.n});
+    } else if (l == 0 && lap_batched<V0>(v0, H)) {
+      if constexpr (std::is_same<V0, LapView>::value)
+        launch(d, k_down_sb<2>, dim3(nblocks(v0.N, BS), (H.nslices + 1) / 2), dim3(BS), 0, v0,
+               (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, active, H.nslices);
     } else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
              RowRange{0, lv.n});

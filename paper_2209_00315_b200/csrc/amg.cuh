@@ -47,6 +47,28 @@ struct LapView {
     }
     f(r, d);
   }
+  // slice-batched kernels: the neighbour slots of kite fc, loaded once and shared by
+  // the rows kk*N + fc of several slices (nb is common to all slices)
+  __device__ __forceinline__ void nbrs(int fc, int (&c)[4]) const {
+#pragma unroll
+    for (int t = 0; t < 4; t++) c[t] = nb[t * N + fc];
+  }
+  // row kk*N + fc with preloaded slots: row()'s entries, values and order exactly
+  template <class F>
+  __device__ __forceinline__ void row_nb(int kk, int fc, const int (&c)[4], F&& f) const {
+    const double* o = off + (size_t)kk * 4 * N + fc;
+    long long base = (long long)kk * N;
+    double d = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      if (c[t] >= 0) {
+        double a = o[(size_t)t * N];
+        d -= a;
+        f(base + c[t], a);
+      }
+    }
+    f(base + fc, d);
+  }
 };
 
 // HSS (NEXT f2): the diagonally scaled, shifted blocks
@@ -251,6 +273,10 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
 // coarsest solve) runs redundantly on every rank on the allgathered input.  Same sums in the
 // same order as amg_vcycle (bitwise equal to the single-GPU cycle).
 class Comm;
+// Slice batching of the level-0 AMG(A) / PCG kernels on LapView (GPU-only launch shape,
+// bitwise-neutral): slices per block, 1 = unbatched.  Env BBOT_LAP_SB (A/B runs).
+int lap_sb();
+bool lap_expl();             // explicit load-phase variants (env BBOT_LAP_SB_EXPL)   // resident CTAs per SM requested (env BBOT_LAP_SB_MINB)
 template <class V0>
 void amg_vcycle_slab(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* x, Comm& comm, int ra, int rb);
 
