@@ -167,6 +167,10 @@ class ByteModel:
         """Kernel name without arguments; the slice-batched level-0 kernels (k_*_sb / _sbx<NS, MINB>,
         NS slices per block) move the bytes of the kernel they batch."""
         base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
+        if base.startswith("k_down_sb<") and base.replace(" ", "").endswith((",false>", ",0>")):
+            return "k_down_nx<LapView>"              # pre-sweep that does not write x (BBOT_LAP_RES)
+        if base == "k_up_dot_res":
+            return "k_up_dot_res<LapView>"
         m = re.match(r"(k_pcg_pq|k_down|k_up_dot)_sbx?<", base)
         return f"{m.group(1)}<LapView>" if m else base
 
@@ -176,7 +180,8 @@ class ByteModel:
             return None
         base = self._base(name)
         a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView>" in base
-        if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict", "k_resid_sk<SellView>", "k_jacobi_sk"):
+        if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict", "k_resid_sk<SellView>", "k_jacobi_sk",
+                    "k_down_nx<SellView>", "k_up_res<SellView>"):
             lv = self._level(grid, by="nc" if base == "k_restrict" else "n")
             a_side = lv is not None and lv[0] == "A"
         return b * self.act if a_side else b
@@ -210,7 +215,9 @@ class ByteModel:
             return 16 * n
         if base == "k_down<LapView>":
             return 32 * n + self.lapA                 # read b dinv, write x r
-        if base in ("k_up_dot<LapView>", "k_up<LapView>"):
+        if base == "k_down_nx<LapView>":
+            return 24 * n + self.lapA                 # read b dinv, write r (x = om D^-1 b is recomputed)
+        if base in ("k_up_dot<LapView>", "k_up<LapView>", "k_up_dot_res<LapView>"):   # _res: r instead of x
             nc1 = self.levA[0][2]
             return 36 * n + 8 * nc1 + self.lapA       # read b x dinv agg(4) xc, write z
         if base == "k_spmv<LapView>":
@@ -221,12 +228,14 @@ class ByteModel:
             return self.tT + 24 * m                   # read b x, write r
         if base == "k_post<SliceEllView>":
             return self.tT + 32 * m                   # read b xt dinv, write out
-        if base in ("k_down<SellView>", "k_up<SellView>"):
+        if base in ("k_down<SellView>", "k_up<SellView>", "k_down_nx<SellView>", "k_up_res<SellView>"):
             lv = self._level(grid)
             if lv is None:
                 return None
             _, _, (nl, nnz, nc) = lv
-            return 12 * nnz + (32 * nl if base.startswith("k_down") else 36 * nl + 8 * nc)
+            if base.startswith("k_down"):
+                return 12 * nnz + (24 if "_nx" in base else 32) * nl
+            return 12 * nnz + 36 * nl + 8 * nc
         if base == "k_restrict":
             lv = self._level(grid, by="nc")
             if lv is None:

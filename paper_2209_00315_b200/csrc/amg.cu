@@ -313,6 +313,31 @@ __global__ void k_down(V v, const double* __restrict__ dinv, const double* __res
   res[r] = acc;
 }
 
+// mode-A coarse levels, BBOT_SELL_RES (the level-0 trick of k_up_dot_res on the SELL levels):
+// the pre-sweep keeps only its residual (x = om D^-1 b is recomputed where needed) and the
+// post-sweep starts from it, b - A (x + P xc) = res - A (P xc): one gather per entry
+// (xc[agg[c]]) instead of two (x[c] too), no x in memory.  Rounding differs from k_up's order.
+template <class V>
+__global__ void k_down_nx(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                          double* __restrict__ res, SliceSkip sk, RowRange rr) {
+  long long r = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rr.r1 || sk.skip(r)) return;
+  double acc = b[r];
+  v.row(r, [&](long long c, double a) { acc -= a * (om * dinv[c] * b[c]); });
+  res[r] = acc;
+}
+template <class V>
+__global__ void k_up_res(V v, const double* __restrict__ dinv, const double* __restrict__ b, double om,
+                         const double* __restrict__ res, const int* __restrict__ agg, const double* __restrict__ xc,
+                         double* __restrict__ xo, SliceSkip sk) {
+  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= v.nrows || sk.skip(r)) return;
+  double acc = res[r];
+  v.row(r, [&](long long c, double a) { acc -= a * xc[agg[c]]; });
+  const double w = om * dinv[r];
+  xo[r] = (w * b[r] + xc[agg[r]]) + w * acc;
+}
+
 __global__ void k_restrict(long long nc, const long long* __restrict__ mptr, const int* __restrict__ midx,
                            const double* __restrict__ r, double* bc, SliceSkip sk, RowRange rr) {
   long long I = rr.r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -447,7 +472,7 @@ int lap_sb() {
   return v == 2 ? 2 : 1;
 }
 
-template <int NS>
+template <int NS, bool WX>
 __global__ void __launch_bounds__(256, 6) k_down_sb(LapView v, const double* __restrict__ dinv,
                                                     const double* __restrict__ b, double om, double* __restrict__ x,
                                                     double* __restrict__ res, const double* __restrict__ active,
@@ -464,9 +489,58 @@ __global__ void __launch_bounds__(256, 6) k_down_sb(LapView v, const double* __r
     const long long r = (long long)kk * v.N + i;
     double acc = b[r];
     v.row_nb(kk, i, c, [&](long long cc, double a) { acc -= a * (om * dinv[cc] * b[cc]); });
-    x[r] = om * dinv[r] * b[r];
+    if (WX) x[r] = om * dinv[r] * b[r];
     res[r] = acc;
   }
+}
+
+// ---- residual-based post sweeps (BBOT_LAP_RES, BBOT_SELL_RES; both on by default)
+int lap_res() {
+  const char* e = getenv("BBOT_LAP_RES");
+  return e ? atoi(e) != 0 : BBOT_LAP_RES_DEFAULT;
+}
+int sell_res() {
+  const char* e = getenv("BBOT_SELL_RES");
+  return e ? atoi(e) != 0 : BBOT_SELL_RES_DEFAULT;
+}
+
+// Level 0 of AMG(A) (LapView): the post sweep from the pre-sweep's residual.  With x = om D^-1 b and
+// res = b - A x (k_down), b - A (x + P xc) = res - A (P xc): the sweep gathers only the
+// coarse correction xc[agg[c]] of the neighbours (4 gathers per kite less, no x in HBM at
+// all: x_r is recomputed from b_r and dinv_r).  Mathematically the same z; rounding differs
+// from k_up_dot's order at the 1e-16 level.
+__global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_up_dot_res(LapView v, const double* __restrict__ dinv,
+                         const double* __restrict__ b, double om, const double* __restrict__ res,
+                         const int* __restrict__ agg, const double* __restrict__ xc, double* __restrict__ xo,
+                         RedArgs R, PcgRzFin fin, const double* active) {
+  const int k = blockIdx.y;
+  long long beg, end;
+  red_chunk(v.N, R.parts, beg, end);
+  if (active && active[k] == 0.0) end = beg;     // converged slice: nothing to do (partial 0)
+  const long long base = (long long)k * v.N;
+  const double* o = v.off + (size_t)k * 4 * v.N;
+  const int* ag = agg + base;
+  double dot = 0.0;
+  for (int fc = (int)beg + threadIdx.x; fc < (int)end; fc += blockDim.x) {
+    const long long r = base + fc;
+    double acc = res[r], dg = 0.0;
+    const double cr = xc[ag[fc]];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int c = v.nb[t * v.N + fc];
+      if (c >= 0) {
+        const double a = o[(size_t)t * v.N + fc];
+        dg -= a;
+        acc -= a * xc[ag[c]];
+      }
+    }
+    acc -= dg * cr;
+    const double br = b[r], w = om * dinv[r];
+    const double z = (w * br + cr) + w * acc;
+    xo[r] = z;
+    dot += br * z;
+  }
+  if (red_commit(dot, R)) fin(R.out);
 }
 
 // level 0 of an AMG(A) hierarchy on the plain cell-ELL view, slice-major rows of N
@@ -1513,12 +1587,22 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
       launch(d, k_jacobi0, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, b, om, lv.x.p, RowRange{0, lv.n});
       launch(d, k_resid<V0>, dim3(nb), dim3(BS), 0, v0, b, (const double*)lv.x.p, lv.r.p, RowRange{0, lv.n});
     } else if (l == 0 && lap_batched<V0>(v0, H)) {
-      if constexpr (std::is_same<V0, LapView>::value)
-        launch(d, k_down_sb<2>, dim3(nblocks(v0.N, BS), (H.nslices + 1) / 2), dim3(BS), 0, v0,
-               (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, active, H.nslices);
+      if constexpr (std::is_same<V0, LapView>::value) {
+        // the residual-based post sweep recomputes x = om D^-1 b: no x in HBM
+        const bool wx = !(fuse && !UP_SPLIT && lap_res() && fuse->L == v0.N);
+        if (wx)
+          launch(d, k_down_sb<2, true>, dim3(nblocks(v0.N, BS), (H.nslices + 1) / 2), dim3(BS), 0, v0,
+                 (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, active, H.nslices);
+        else
+          launch(d, k_down_sb<2, false>, dim3(nblocks(v0.N, BS), (H.nslices + 1) / 2), dim3(BS), 0, v0,
+                 (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, active, H.nslices);
+      }
     } else if (l == 0)
       launch(d, k_down<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, lv.x.p, lv.r.p, skip_at(0),
              RowRange{0, lv.n});
+    else if (H.mode != 1 && sell_res())
+      launch(d, k_down_nx<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
+             (const double*)lv.b.p, om, lv.r.p, skip_at(l), RowRange{0, lv.n});
     else if (DOWN_SPLIT) {
       launch(d, k_jacobi_sk, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.dinv.p, (const double*)lv.b.p, om,
              lv.x.p, skip_at(l));
@@ -1551,6 +1635,10 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
              skip_at(0), RowRange{0, lv.n});
       launch(d, k_post_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.xt.p, out, fuse->L, fuse->R, fuse->fin, active);
+    } else if (l == 0 && fuse && lap_batched<V0>(v0, H) && lap_res() && fuse->L == lv.n / H.nslices) {
+      if constexpr (std::is_same<V0, LapView>::value)
+        launch(d, k_up_dot_res, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
+               (const double*)lv.r.p, (const int*)lv.agg.p, xc, out, fuse->R, fuse->fin, active);
     } else if (l == 0 && fuse) {
       launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);
@@ -1562,6 +1650,9 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
     } else if (l == 0) {
       launch(d, k_up<V0>, dim3(nb), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om, (const double*)lv.x.p,
              (const int*)lv.agg.p, xc, out, skip_at(0));
+    } else if (H.mode != 1 && sell_res()) {
+      launch(d, k_up_res<SellView>, dim3(nb), dim3(BS), 0, lv.sell(), (const double*)lv.dinv.p,
+             (const double*)lv.b.p, om, (const double*)lv.r.p, (const int*)lv.agg.p, xc, out, skip_at(l));
     } else if (H.mode == 1 && SELL_SPLIT) {   // T coarse level: prolongate into r (free here), then sweep
       launch(d, k_prolong, dim3(nb), dim3(BS), 0, lv.n, (const double*)lv.x.p, (const int*)lv.agg.p, xc, lv.r.p,
              SliceSkip{nullptr, nullptr, 1}, RowRange{0, lv.n});

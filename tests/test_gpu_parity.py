@@ -109,6 +109,34 @@ def test_bb_apply_parity(name, kw):
     assert _rel(zg, zo) < 1e-8
 
 
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_residual_based_post_sweep_equals_classic(name):
+    """AMG(A) post sweeps from the pre-sweep's residual (csrc/amg.cu k_up_dot_res / k_up_res:
+    b - A(x + P xc) = res - A P xc, x = om D^-1 b recomputed, the default) against the classic
+    sweeps on x + P xc (BBOT_LAP_RES = BBOT_SELL_RES = 0): the same BB apply to rounding level,
+    identical inner counts.  (Both are held to the oracle by test_bb_apply_parity; this pins the
+    algebraic identity itself, incl. the K-cycle tail on C2's forced deep hierarchy elsewhere.)"""
+    import os
+    pb, p, d, ctx, _ = _setup(name)
+    ctx.set_exec_mode(False)            # eager: the knobs are read at every launch
+    ctx.assemble()
+    r = np.random.default_rng(11).standard_normal(d.n + d.m)
+    r[d.n:] = d.P(r[d.n:])
+    out = {}
+    try:
+        for res in ("0", "1"):
+            os.environ.update(BBOT_LAP_RES=res, BBOT_SELL_RES=res)
+            out[res] = ctx.bb_apply(r)
+    finally:
+        os.environ.pop("BBOT_LAP_RES", None)
+        os.environ.pop("BBOT_SELL_RES", None)
+    (z0, t0, a0), (z1, t1, a1) = out["0"], out["1"]
+    assert (t0, a0) == (t1, a1)
+    assert _rel(z1, z0) < 1e-10, _rel(z1, z0)
+    if name == "C2":
+        assert not np.array_equal(z1, z0)     # the knob really switches kernels (rounding differs)
+
+
 _IPM_CACHE = {}
 
 
