@@ -169,8 +169,9 @@ class ByteModel:
         base = name.split("(")[0].replace("void ", "").replace("bbot::", "")
         if base.startswith("k_down_sb<") and base.replace(" ", "").endswith((",false>", ",0>")):
             return "k_down_nx<LapView>"              # pre-sweep that does not write x (BBOT_LAP_RES)
-        if base == "k_up_dot_res":
-            return "k_up_dot_res<LapView>"
+        if base.startswith("k_up_dot_res"):           # <true>: 1/diag recomputed from the slots (no dinv read)
+            return "k_up_dot_res<LapView,nodinv>" if base.replace(" ", "").endswith(("<true>", "<1>")) \
+                else "k_up_dot_res<LapView>"
         m = re.match(r"(k_pcg_pq|k_down|k_up_dot)_sbx?<", base)
         return f"{m.group(1)}<LapView>" if m else base
 
@@ -179,7 +180,7 @@ class ByteModel:
         if b is None:
             return None
         base = self._base(name)
-        a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView>" in base
+        a_side = base.startswith(("k_pcg_", "k_tailA")) or "<LapView" in base
         if base in ("k_down<SellView>", "k_up<SellView>", "k_restrict", "k_resid_sk<SellView>", "k_jacobi_sk",
                     "k_down_nx<SellView>", "k_up_res<SellView>"):
             lv = self._level(grid, by="nc" if base == "k_restrict" else "n")
@@ -217,6 +218,8 @@ class ByteModel:
             return 32 * n + self.lapA                 # read b dinv, write x r
         if base == "k_down_nx<LapView>":
             return 24 * n + self.lapA                 # read b dinv, write r (x = om D^-1 b is recomputed)
+        if base == "k_up_dot_res<LapView,nodinv>":
+            return 28 * n + 8 * self.levA[0][2] + self.lapA      # read b r agg(4) xc, write z
         if base in ("k_up_dot<LapView>", "k_up<LapView>", "k_up_dot_res<LapView>"):   # _res: r instead of x
             nc1 = self.levA[0][2]
             return 36 * n + 8 * nc1 + self.lapA       # read b x dinv agg(4) xc, write z
@@ -340,9 +343,11 @@ def ncu_traffic(config, kernel):
     try:
         summ = json.load(open(NCU_SUMMARY))
         per = summ["dram_bytes_per_launch"][config]
-        short = kernel.replace("void ", "").replace("bbot::", "")
+        norm = lambda t: (t.replace("void ", "").replace("bbot::", "").replace("true", "1")
+                          .replace("false", "0").replace(" ", ""))      # ncu prints bool template args as 0/1
+        short = norm(kernel)
         for k, v in per.items():
-            if k.replace("void ", "").replace("bbot::", "") == short:
+            if norm(k) == short:
                 return v, summ.get("round", {}).get(f"{config}/{k}", "r1")
     except Exception:
         pass

@@ -499,6 +499,10 @@ int lap_res() {
   const char* e = getenv("BBOT_LAP_RES");
   return e ? atoi(e) != 0 : BBOT_LAP_RES_DEFAULT;
 }
+int lap_rdinv() {
+  const char* e = getenv("BBOT_LAP_RDINV");
+  return e ? atoi(e) != 0 : BBOT_LAP_RDINV_DEFAULT;
+}
 int sell_res() {
   const char* e = getenv("BBOT_SELL_RES");
   return e ? atoi(e) != 0 : BBOT_SELL_RES_DEFAULT;
@@ -509,6 +513,7 @@ int sell_res() {
 // coarse correction xc[agg[c]] of the neighbours (4 gathers per kite less, no x in HBM at
 // all: x_r is recomputed from b_r and dinv_r).  Mathematically the same z; rounding differs
 // from k_up_dot's order at the 1e-16 level.
+template <bool RDINV>
 __global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_up_dot_res(LapView v, const double* __restrict__ dinv,
                          const double* __restrict__ b, double om, const double* __restrict__ res,
                          const int* __restrict__ agg, const double* __restrict__ xc, double* __restrict__ xo,
@@ -535,7 +540,8 @@ __global__ void __launch_bounds__(256, BBOT_LAP_MINB) k_up_dot_res(LapView v, co
       }
     }
     acc -= dg * cr;
-    const double br = b[r], w = om * dinv[r];
+    // RDINV: dinv[r] = 1 / (sum of the slots, in slot order) is k_dinv's value exactly
+    const double br = b[r], w = om * (RDINV ? 1.0 / dg : dinv[r]);
     const double z = (w * br + cr) + w * acc;
     xo[r] = z;
     dot += br * z;
@@ -1636,9 +1642,14 @@ bool amg_vcycle(Dev& d, AmgHierarchy& H, const V0& v0, const double* b, double* 
       launch(d, k_post_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.xt.p, out, fuse->L, fuse->R, fuse->fin, active);
     } else if (l == 0 && fuse && lap_batched<V0>(v0, H) && lap_res() && fuse->L == lv.n / H.nslices) {
-      if constexpr (std::is_same<V0, LapView>::value)
-        launch(d, k_up_dot_res, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
-               (const double*)lv.r.p, (const int*)lv.agg.p, xc, out, fuse->R, fuse->fin, active);
+      if constexpr (std::is_same<V0, LapView>::value) {
+        if (lap_rdinv())
+          launch(d, k_up_dot_res<true>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b,
+                 om, (const double*)lv.r.p, (const int*)lv.agg.p, xc, out, fuse->R, fuse->fin, active);
+        else
+          launch(d, k_up_dot_res<false>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b,
+                 om, (const double*)lv.r.p, (const int*)lv.agg.p, xc, out, fuse->R, fuse->fin, active);
+      }
     } else if (l == 0 && fuse) {
       launch(d, k_up_dot<V0>, dim3(fuse->parts, fuse->ns), dim3(BS), 0, v0, (const double*)lv.dinv.p, b, om,
              (const double*)lv.x.p, (const int*)lv.agg.p, xc, out, fuse->L, fuse->R, fuse->fin, active);

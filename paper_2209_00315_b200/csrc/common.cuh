@@ -21,9 +21,13 @@
 #define BBOT_LAP_MINB 8
 #endif
 // residual-based post sweeps of AMG(A) (amg.cu: k_up_dot_res, k_up_res): defaults of the
-// BBOT_LAP_RES (level 0) and BBOT_SELL_RES (SELL levels) knobs
+// BBOT_LAP_RES (level 0), BBOT_SELL_RES (SELL levels) and BBOT_LAP_RDINV (level 0: 1/diag
+// recomputed from the row's slots instead of read) knobs
 #ifndef BBOT_LAP_RES_DEFAULT
 #define BBOT_LAP_RES_DEFAULT 1
+#endif
+#ifndef BBOT_LAP_RDINV_DEFAULT
+#define BBOT_LAP_RDINV_DEFAULT 1
 #endif
 #ifndef BBOT_SELL_RES_DEFAULT
 #define BBOT_SELL_RES_DEFAULT 1

@@ -17,8 +17,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-# (BBOT_LAP_RES, BBOT_SELL_RES)
-VARIANTS = [("0", "0"), ("1", "0"), ("1", "1"), ("0", "0")]
+# (BBOT_LAP_RES, BBOT_SELL_RES, BBOT_LAP_RDINV)
+VARIANTS = [("1", "1", "0"), ("1", "1", "1"), ("1", "1", "0"), ("1", "1", "1")]
 
 
 def main():
@@ -34,8 +34,8 @@ def main():
     ctx = pb.Context(p.verts, p.tris, p.K, p.rho_in, p.rho_f)
     ctx.set_exec_mode(False)
     ref = None
-    for sb, mb in VARIANTS:
-        os.environ.update(BBOT_LAP_RES=sb, BBOT_SELL_RES=mb)
+    for sb, mb, rd in VARIANTS:
+        os.environ.update(BBOT_LAP_RES=sb, BBOT_SELL_RES=mb, BBOT_LAP_RDINV=rd)
         ctx.set_state(phi, rho, s, 1.0)
         ctx.assemble()
         torch.cuda.synchronize()
@@ -51,7 +51,7 @@ def main():
         top = {k: v for k, v in prof.items() if any(x in k for x in ("k_up_dot", "k_pcg_pq", "k_down", "k_pcg_xr"))
                or "Sell" in k or "k_restrict" in k or "k_tailA" in k}
         tot = sum(v[1] for v in prof.values())
-        print(f"LAP_RES={sb} SELL_RES={mb}: solve {dt * 1e3:.0f} ms (kernels {tot:.0f} ms) outer {st['outer_its']} "
+        print(f"LAP_RES={sb} SELL_RES={mb} RDINV={rd}: solve {dt * 1e3:.0f} ms (kernels {tot:.0f} ms) outer {st['outer_its']} "
               f"bitwise={same}", flush=True)
         for k, (n, ms) in sorted(top.items(), key=lambda kv: -kv[1][1]):
             print(f"    {k[:60]:60s} {n:6d} {ms:9.1f} ms", flush=True)
