@@ -57,3 +57,44 @@ def test_reference_arm_rank0_only():
     assert len(lines) == 1
     j = json.loads(lines[0])
     assert j["impl"] == "reference" and j["value"] > 0 and j["cpu_baseline"]["cores"] == 1
+
+
+def test_byte_model_covers_the_level0_kernel_variants():
+    """bench.ByteModel (host logic): every name the level-0 AMG(A) kernels are launched under
+    maps to a byte model, the residual-based variants to the smaller ones (DESIGN.md §5:
+    k_down_sb<2,false> writes no x: 24n instead of 32n vector bytes; k_up_dot_res<true> reads
+    neither x nor dinv: 28n instead of 36n), and ncu's 0/1 spelling of bool template
+    arguments finds the same ncu_summary.json entry as the runtime's true/false."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class Ctx:
+        n, m, N, K, nbar, NE = 129 * 3000, 128 * 1000, 3000, 128, 1000, 6000
+
+        def T_nnz(self):
+            return 27 * self.m, 10
+
+        def amg_levels(self, which):
+            return [(self.n, 5 * self.n, self.n // 4), (self.n // 4, 2 * self.n, 0)], 0
+
+    st = {"outer_its": 28, "inner_T_its": 553, "inner_A_its_total": 100}
+    bm = bench.ByteModel(Ctx(), st)
+    n, lap = Ctx.n, 32 * Ctx.n + 16 * Ctx.N
+    nc1 = Ctx.n // 4
+    cases = {
+        "void bbot::k_down_sb<2, true>(bbot::LapView, double const*)": 32 * n + lap,
+        "void bbot::k_down_sb<2, false>(bbot::LapView, double const*)": 24 * n + lap,
+        "void bbot::k_up_dot<bbot::LapView>(bbot::LapView)": 36 * n + 8 * nc1 + lap,
+        "void bbot::k_up_dot_res<false>(bbot::LapView)": 36 * n + 8 * nc1 + lap,
+        "void bbot::k_up_dot_res<true>(bbot::LapView)": 28 * n + 8 * nc1 + lap,
+        "void bbot::k_pcg_pq<bbot::LapView>(bbot::LapView, long long)": 40 * n + lap,
+    }
+    for name, want in cases.items():
+        assert bm._bytes(name, 0) == want, name
+    g1 = (Ctx.n // 4 + 255) // 256
+    assert bm._bytes("void bbot::k_down_nx<bbot::SellView>(x)", g1) == 12 * 2 * n + 24 * (n // 4)
+    assert bm._bytes("void bbot::k_down<bbot::SellView>(x)", g1) == 12 * 2 * n + 32 * (n // 4)
+    assert bm._bytes("void bbot::k_up_res<bbot::SellView>(x)", g1) == 12 * 2 * n + 36 * (n // 4)
+    a, _ = bench.ncu_traffic("C4", "void bbot::k_up_dot_res<true>")
+    b, _ = bench.ncu_traffic("C4", "void k_up_dot_res<1>")
+    assert a is not None and a == b

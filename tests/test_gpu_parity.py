@@ -332,10 +332,10 @@ def test_ipm_parity_C1_full():
 
 
 def test_ipm_parity_C2_to_mu7():
-    """BASELINE configs[1] (C2: 8192 cells on the jittered mesh, K = 32, 1.07 M unknowns, the
-    AMG(T) time blocks of A42 active) over its first seven mu values, mu 1 -> 2^-7 (A17-A20),
+    """BASELINE configs[1] (C2: 8192 cells on the jittered mesh, K = 32, 1.07 M unknowns)
+    over its first eight mu values, mu 1 -> 2^-7 (A17-A20, A14' from mu < 0.3),
     against the oracle's own run stored in tests/golden/ipm_C2_mu7.json
-    (scripts/oracle_ipm_golden.py C2 0.0078125, oracle only; ~1 h on one core): same
+    (scripts/oracle_ipm_golden.py C2 0.0078125, oracle only; ~2.5 h on one core): same
     systems, trajectory, kinetic energy to 1e-6."""
     import json
     import os
