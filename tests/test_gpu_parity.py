@@ -331,15 +331,23 @@ def test_ipm_parity_C1_full():
     _ipm_compare(log, gold["systems"], st, gold["kinetic_energy"])
 
 
-def test_ipm_parity_C2_to_mu7():
+def _c2_goldens():
+    import glob
+    import os
+    return sorted(os.path.basename(f) for f in
+                  glob.glob(os.path.join(os.path.dirname(__file__), "golden", "ipm_C2_mu*.json")))
+
+
+@pytest.mark.parametrize("gold_file", _c2_goldens() or ["ipm_C2_mu7.json"])
+def test_ipm_parity_C2_first_mus(gold_file):
     """BASELINE configs[1] (C2: 8192 cells on the jittered mesh, K = 32, 1.07 M unknowns)
-    over its first eight mu values, mu 1 -> 2^-7 (A17-A20, A14' from mu < 0.3),
-    against the oracle's own run stored in tests/golden/ipm_C2_mu7.json
-    (scripts/oracle_ipm_golden.py C2 0.0078125, oracle only; ~2.5 h on one core): same
-    systems, trajectory, kinetic energy to 1e-6."""
+    over its first mu values, mu 1 -> 2^-j (A17-A20, A14' from mu < 0.3), against the oracle's
+    own run stored in tests/golden/ipm_C2_mu<j>.json (scripts/oracle_ipm_golden.py C2 2^-j,
+    oracle only; j = 3: ~1 h, j = 7: ~3 h on one core): same systems, trajectory, kinetic
+    energy to 1e-6."""
     import json
     import os
-    path = os.path.join(os.path.dirname(__file__), "golden", "ipm_C2_mu7.json")
+    path = os.path.join(os.path.dirname(__file__), "golden", gold_file)
     if not os.path.exists(path):
         pytest.skip("golden file not generated")
     gold = json.load(open(path))
