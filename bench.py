@@ -475,7 +475,17 @@ def cpu_baseline_from(orc, head_unknowns):
     if orc is None:
         return None
     ups = orc["n_plus_m"] / orc["total_s"]
+    full = None
+    try:      # the oracle's own full C4 solve (scripts/oracle_counts.py, offline, one core): context
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_counts.json"))).get("C4/init/mu=1")
+        if g:
+            full = {"seconds_1core": g["seconds_1core"], "solves_per_s": 1.0 / g["seconds_1core"],
+                    "outer_its": g["outer_its"], "inner_T_its": g["inner_T_its"],
+                    "source": "tests/golden/oracle_counts.json (the oracle's whole C4 step: setup + BB-FGMRES to 1e-10, run offline on one core)"}
+    except Exception:
+        pass
     return {"value": ups / head_unknowns, "unit": "solves/s", "cores": 1, "kind": "oracle",
+            "oracle_full_C4_solve": full,
             "sample": (f"the oracle's full solve of the {orc['config']} mu=1 Newton system (setup {orc['setup_s']:.1f} s "
                        f"+ BB-FGMRES {orc['solve_s']:.1f} s, {orc['outer_its']} outer iterations, eps_out=1e-10) "
                        f"on 1 host core, run concurrently with the GPU legs = {ups:.0f} unknowns/s, divided by the "

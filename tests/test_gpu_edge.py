@@ -143,7 +143,7 @@ def test_C3_direction_satisfies_newton_system():
 def test_C4_first_system_counts_match_oracle():
     """The bench headline system (BASELINE configs[3], C4: 131 072 cells, K = 128, 67.5 M
     unknowns): the GPU's first IPM Newton solve converges with the oracle's own outer count
-    +-1 (tests/golden/oracle_counts.json: scripts/oracle_counts.py, oracle only, ~2 h and
+    +-1 (tests/golden/oracle_counts.json: scripts/oracle_counts.py, oracle only, 7094 s and
     ~30 GB on one core) and the same inner T-GMRES count within the +-1 outer slack."""
     import json
     import os
@@ -162,3 +162,9 @@ def test_C4_first_system_counts_match_oracle():
     assert o["converged"] and st["converged"] == 1
     assert abs(st["outer_its"] - o["outer_its"]) <= 1, (st, o)
     assert abs(st["inner_T_its"] - o["inner_T_its"]) <= 50, (st, o)
+    if st["outer_its"] == o["outer_its"]:
+        # same iterate on both sides: the FGMRES residual estimate and the per-slice PCG work agree
+        # (measured: counts 28 / 553 on both sides, PCG slice-iterations 123 213 vs 123 193,
+        # relative residuals 5.46331e-11 vs 5.46332e-11)
+        assert abs(st["rel_res"] - o["rel_res"]) <= 1e-3 * o["rel_res"], (st["rel_res"], o["rel_res"])
+        assert abs(st["inner_A_its_total"] - o["inner_A_its_total"]) <= 0.01 * o["inner_A_its_total"], (st, o)
